@@ -1,0 +1,336 @@
+#!/usr/bin/env python3
+"""Benchmark: CDF 9/7 forward 2-D DWT, Gpixel/s and HBM roofline on B200.
+
+Workload (BASELINE.json configs[3], the north-star target): non-separable
+lifting, optimized (paper's 36 ops/quad), CDF 9/7, float32, 8-level Mallat
+pyramid of a 16384 x 16384 image per GPU. One step = one full 8-level
+forward pyramid (8 fused level kernels) of the resident image.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): weak scaling, each rank transforms its
+own 16384-row strip of a 16384 x (16384 N) image; rank 0 prints the line.
+
+Timing: W untimed warm-up steps; the K timed steps are one CUDA graph
+(captured with an event between every level) replayed between a barrier +
+synchronize on both sides; CUDA events on the launching stream give the
+step time and every level kernel's duration; max over ranks. The image is
+1 GiB, larger than the 126 MB L2, so the level-1 input always streams from
+HBM (no explicit flush). nvidia-smi samples clocks during the timed region.
+
+Metric and traffic model: pixels of the original image per second, and the
+reference's own traffic model of 8 B per pixel per level (read + write
+float32, proj/src/bench.cpp:84-85), i.e. 10.667 B per original pixel for 8
+levels. roofline: the level-1 kernel (the dominant launch) at 8 B/pixel over
+its measured duration vs the measured copy bandwidth in MEASURED_PEAKS.json.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WAVELET, SCHEME, OPTIMIZED = "cdf97", "nonseparable-lifting", True
+SIZE, LEVELS = 16384, 8
+METRIC = "CDF 9/7 2-D DWT Gpixel/s (ns/pixel) and achieved HBM GB/s vs peak, 1/2/4/8 GPU"
+# CPU baseline sample: a 16384 x 2048 row band of the same image, 8 levels
+SAMPLE_ROWS = 2048
+
+
+def workload_config(n):
+    return {
+        "workload": f"CDF 9/7 non-separable lifting (optimized, 36 ops/quad) forward 8-level Mallat "
+                    f"pyramid, {SIZE}x{SIZE} float32 per GPU (BASELINE configs[3])",
+        "wavelet": WAVELET, "scheme": SCHEME, "optimized": OPTIMIZED,
+        "image": [SIZE, SIZE * n], "levels": LEVELS, "extension": "periodic",
+        "parallelism": f"row-strips x{n}" if n > 1 else "single GPU",
+        "l2": "inputs larger than L2 (1 GiB image per GPU vs 126 MB L2), no flush",
+        "traffic_model": "8 B/pixel/level (reference bench.cpp:84-85)",
+    }
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per level-1 launch from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "ncu_level1_summary.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index=0):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.1)
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for n, v in zip(names, r[2:6]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    n = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return n, rank, local
+
+
+def cpu_reference(steps, warmup, workers=None):
+    """Reference CPU implementation (oracle/_ref, compiled from the reference
+    sources) on a bounded sample: a 16384 x SAMPLE_ROWS band, 8 levels."""
+    from oracle import ref as R
+    from oracle import dwt_oracle as O
+    workers = workers or os.cpu_count() or 1
+    img = O.random_image(SIZE, SAMPLE_ROWS, 1)
+    times = []
+    for i in range(warmup + steps):
+        t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=workers, repeats=1)
+        if i >= warmup:
+            times.append(t)
+    t = statistics.median(times)
+    gpix = SIZE * SAMPLE_ROWS / t / 1e9
+    return {"value": gpix, "unit": "Gpixel/s", "cores": workers, "kind": "reference",
+            "sample": f"{SIZE}x{SAMPLE_ROWS} band of the LCG image, {LEVELS}-level Mallat loop over the "
+                      f"reference compile/run API (oracle/_ref, reference sources, -O3), workers={workers}, "
+                      f"median of {len(times)}", "seconds": t}
+
+
+def run_reference_arm(args):
+    n, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    cb = cpu_reference(args.steps, args.warmup)
+    v = cb["value"]
+    line = {
+        "metric": METRIC, "value": v, "unit": "Gpixel/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference LCG image, seed 1)",
+        "config": workload_config(n), "impl": "reference",
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1704_08657_b200 as dwt
+    from paper_1704_08657_b200.synth import random_image
+
+    n, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if n > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    plan = dwt.Plan(WAVELET, SCHEME, optimized=OPTIMIZED)
+    W = H = SIZE
+    # this rank's strip: rows [rank*H, (rank+1)*H) of the W x (n*H) image
+    img = random_image(W, H * n, 1, row0=rank * H, rows=H, device=dev)
+    out = torch.empty_like(img)
+    scratch = torch.empty(dwt.workspace_bytes(W, H, LEVELS) // 4 + 64, dtype=torch.float32, device=dev)
+
+    # per-level views: LL_l lives in scratch (ping-pong), bands in the Mallat buffer
+    def level_views():
+        views = []
+        src = img
+        a_elems = (W // 2) * (H // 2)
+        a_pad = (a_elems + 63) // 64 * 64
+        for lvl in range(1, LEVELS + 1):
+            w, h = W >> (lvl - 1), H >> (lvl - 1)
+            w2, h2 = w // 2, h // 2
+            if lvl == LEVELS:
+                ll = out[:h2, :w2]
+            else:
+                base = 0 if lvl % 2 == 1 else a_pad
+                ll = scratch[base:base + w2 * h2].view(h2, w2)
+            bands = [ll, out[:h2, w2:w], out[h2:h, :w2], out[h2:h, w2:w]]
+            views.append((src, bands))
+            src = ll
+        return views
+
+    views = level_views()
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(events=None):
+        for lvl, (src, bands) in enumerate(views):
+            if events is not None:
+                events[lvl].record(stream)
+            plan.forward_level(src, bands, stream=stream.cuda_stream)
+        if events is not None:
+            events[LEVELS].record(stream)
+
+    # warm-up (also proves the multi-level API gives the same bits)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    stream.synchronize()
+    ref_out = plan.forward_mallat(img, LEVELS, scratch=scratch)
+    torch.cuda.synchronize()
+    assert torch.equal(ref_out, out), "per-level driver and forward_mallat disagree"
+
+    # capture K steps with per-level events into one graph
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(LEVELS + 1)] for _ in range(args.steps)]
+    graph = torch.cuda.CUDAGraph()
+    launches0 = dwt.launch_count()
+    with torch.cuda.graph(graph, stream=stream):
+        for k in range(args.steps):
+            step(evs[k])
+    launches_captured = dwt.launch_count() - launches0
+    graph.replay()  # untimed replay warms the graph
+    torch.cuda.synchronize()
+
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if n > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        graph.replay()
+        t1.record(stream)
+        t1.synchronize()
+        if n > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    level_ms = [statistics.mean(e[l].elapsed_time(e[l + 1]) for e in evs) for l in range(LEVELS)]
+    if n > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    pixels = W * H * n
+    value = pixels / (ms_per_step * 1e-3) / 1e9
+
+    # end to end through the C ABI host entry point: pinned host image ->
+    # H2D -> 8 levels -> D2H of the whole pyramid, synchronous per step
+    host_img = img.cpu().pin_memory()
+    host_out = torch.empty_like(host_img).pin_memory()
+    hi, ho = host_img.numpy(), host_out.numpy()
+    plan.forward_mallat_host(hi, LEVELS, ho)
+    if n > 1:
+        dist.barrier()
+    e2e_t = []
+    for _ in range(args.e2e_steps):
+        a = time.perf_counter()
+        plan.forward_mallat_host(hi, LEVELS, ho)
+        e2e_t.append(time.perf_counter() - a)
+    e2e_s = statistics.median(e2e_t)
+    if n > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert torch.equal(host_out.to(dev), out), "host entry point disagrees with device pyramid"
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        l1_bytes = 8.0 * W * H
+        achieved = l1_bytes / (level_ms[0] * 1e-3) / 1e9
+        pyr_bytes = sum(8.0 * (W >> l) * (H >> l) for l in range(LEVELS))
+        cpu = None
+        if not args.no_cpu_baseline:
+            try:
+                cb = cpu_reference(steps=3, warmup=1)
+                cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # oracle not built on this box
+                cpu = {"value": None, "unit": "Gpixel/s", "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference LCG random_image, seed 1, generated on device with jump-ahead)",
+            "config": workload_config(n),
+            "ns_per_pixel": ms_per_step * 1e6 / pixels,
+            "pyramid_hbm_gbs": pyr_bytes * n / (ms_per_step * 1e-3) / 1e9 / n,
+            "levels_ms": [round(x, 5) for x in level_ms],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "level 1 (16384^2 -> 4 x 8192^2), 8 B/pixel algorithmic",
+                         "peak_source": peak_src},
+            "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
+                    "h2d_bytes_per_step": int(W * H * 4), "d2h_bytes_per_step": int(W * H * 4),
+                    "api": "dwt2d_forward_mallat_host (C ABI), pinned host buffers"},
+            "gpu_launches": int(launches_captured),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if n > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * dwt2d_b200 — C ABI of the B200-native 2-D DWT (arXiv 1704.08657 schemes).
+ *
+ * This is the drop-in boundary for the reference's transform path. The
+ * reference exposes it as header-only C++ templates with no FFI
+ * (reference: proj/include/dwt2d/executor.hpp:52-53 compile<T>, :196-197
+ * run<T>, :242-244 inverse_lifting<T>; scheme.hpp:76-92 builders;
+ * wavelet.hpp:37-45 wavelet lookup). Every entry point below replaces one of
+ * those calls (cited per function); the C++ mirror of the reference API in
+ * include/dwt2d_b200/executor.hpp is written on top of these functions.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; device pointers unless a name says _host
+ *  - pitches are in float elements (not bytes)
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream)
+ *  - every function returns a dwt2d_status; on failure dwt2d_last_error()
+ *    returns a thread-local message (no exceptions cross the ABI; the C++
+ *    layer rethrows DWT2D_EINVAL as std::invalid_argument like the reference)
+ *  - a plan is immutable after creation and may be used from several
+ *    threads/streams at once (unlike the reference's ExecPlan, whose
+ *    barrier_count run() mutates, executor.hpp:211-225)
+ */
+#ifndef DWT2D_B200_H
+#define DWT2D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DWT2D_B200_API __attribute__((visibility("default")))
+
+typedef enum {
+  DWT2D_OK = 0,
+  DWT2D_EINVAL = 1,      /* invalid argument (reference: std::invalid_argument) */
+  DWT2D_ECUDA = 2,       /* CUDA runtime error */
+  DWT2D_ENOMEM = 3,      /* device or host allocation failed */
+  DWT2D_EUNSUPPORTED = 4 /* no compiled kernel for this lowered program */
+} dwt2d_status;
+
+/* reference SchemeKind, scheme.hpp:13-20 (same order) */
+typedef enum {
+  DWT2D_SEPARABLE_CONVOLUTION = 0,
+  DWT2D_SEPARABLE_LIFTING = 1,
+  DWT2D_NONSEPARABLE_CONVOLUTION = 2,
+  DWT2D_NONSEPARABLE_POLYCONVOLUTION = 3,
+  DWT2D_NONSEPARABLE_LIFTING = 4,
+  DWT2D_INVERSE_LIFTING = 5
+} dwt2d_scheme;
+
+/* reference Extension, image.hpp:10 */
+typedef enum { DWT2D_PERIODIC = 0, DWT2D_SYMMETRIC = 1 } dwt2d_extension;
+
+/* how fused groups become kernel sub-steps (see include/dwt2d_b200/lowering.hpp) */
+typedef enum {
+  DWT2D_LOWERING_DEFAULT = 0,  /* composed for baseline, factored for optimized */
+  DWT2D_LOWERING_COMPOSED = 1, /* reference tap order: bit-faithful arithmetic */
+  DWT2D_LOWERING_FACTORED = 2  /* one sub-step per factor: paper's op count */
+} dwt2d_lowering;
+
+typedef struct {
+  const char* wavelet; /* built-in name or definition-file path (wavelet.cpp:226-232) */
+  int scheme;          /* dwt2d_scheme */
+  int optimized;       /* apply optimize_constant_split (scheme.cpp:279-378) */
+  int extension;       /* dwt2d_extension */
+  int lowering;        /* dwt2d_lowering */
+  int workers;         /* reference compile() contract: must be >= 1 (executor.hpp:54-55);
+                          the GPU ignores it */
+} dwt2d_plan_desc;
+
+/* One lowered sub-step program as plain tables (what the kernels execute). */
+typedef struct {
+  int32_t identity; /* output component copies the input component */
+  int32_t tap_begin, tap_end;
+  float scale;
+} dwt2d_row;
+
+typedef struct {
+  int32_t comp, dm, dn; /* reads component `comp` at (x + dm, y + dn) */
+  float w;
+} dwt2d_tap;
+
+typedef struct {
+  int32_t nsteps;          /* sub-steps */
+  const dwt2d_row* rows;   /* nsteps * 4 */
+  int32_t ntaps;
+  const dwt2d_tap* taps;
+  int32_t logical_steps;   /* count_steps(scheme): the reference's barrier count */
+  int32_t extension;       /* dwt2d_extension */
+  int32_t forward;         /* 1 forward analysis, 0 inverse synthesis */
+} dwt2d_program;
+
+typedef struct dwt2d_plan dwt2d_plan;
+
+typedef struct {
+  char key[96];             /* "<wavelet>/<scheme>/<base|opt>/<lowering>" */
+  uint64_t fingerprint;     /* hash of the tap tables */
+  int32_t logical_steps;    /* count_steps: reference barrier count */
+  int32_t substeps;         /* sub-steps fused into one pass per level */
+  int64_t operations;       /* count_operations (paper Table 1) */
+  int64_t taps_per_quad;    /* multiply-adds per 2x2 quad executed by the kernel */
+  int32_t reach_left, reach_right, reach_up, reach_down; /* component-grid halo */
+  int32_t columns_per_lane; /* CW of the level kernel */
+  int32_t forward;
+  int32_t extension;
+} dwt2d_plan_info;
+
+/* --- plans -------------------------------------------------------------- */
+
+/* build_scheme/optimize_constant_split/build_inverse_lifting + compile<float>
+ * (scheme.cpp:244-378, executor.hpp:52-103) */
+DWT2D_B200_API int dwt2d_plan_create(const dwt2d_plan_desc* desc, dwt2d_plan** plan);
+/* compile<float> of an arbitrary lowered program (the C++ compile() path) */
+DWT2D_B200_API int dwt2d_plan_create_from_program(const dwt2d_program* prog, dwt2d_plan** plan);
+DWT2D_B200_API void dwt2d_plan_destroy(dwt2d_plan* plan);
+DWT2D_B200_API int dwt2d_plan_get_info(const dwt2d_plan* plan, dwt2d_plan_info* info);
+/* The lowered tables the plan's kernel executes (rows: nsteps*4, taps),
+ * the same layout as dwt2d_program. Pass NULL buffers to query counts. */
+DWT2D_B200_API int dwt2d_plan_get_tables(const dwt2d_plan* plan, dwt2d_row* rows, int32_t rows_cap,
+                                         dwt2d_tap* taps, int32_t taps_cap, int32_t* nrows,
+                                         int32_t* ntaps);
+/* describe() text of the plan's scheme (scheme.cpp:416-454); desc plans only */
+DWT2D_B200_API int dwt2d_plan_describe(const dwt2d_plan* plan, char* buf, size_t len);
+
+/* --- single level, device buffers ------------------------------------------ */
+
+/* run<float>(plan, PolyphaseImage) on four device component planes
+ * (executor.hpp:196-238): in[j], out[j] are w2 x h2 with pitches in floats. */
+DWT2D_B200_API int dwt2d_run_planar(const dwt2d_plan* plan, const float* const in[4],
+                                    const size_t in_pitch[4], float* const out[4],
+                                    const size_t out_pitch[4], int w2, int h2, void* stream);
+
+/* One forward level straight from an interleaved W x H image (polyphase_split
+ * fused into the load, image.hpp:73-94): out[j] are the four W/2 x H/2 bands
+ * LL (ee), HL (oe), LH (eo), HH (oo). */
+DWT2D_B200_API int dwt2d_forward_level(const dwt2d_plan* plan, const float* image, size_t pitch,
+                                       int width, int height, float* const out[4],
+                                       const size_t out_pitch[4], void* stream);
+
+/* One inverse level into an interleaved W x H image (polyphase_merge fused
+ * into the store, image.hpp:96-113). `plan` must be an inverse plan. */
+DWT2D_B200_API int dwt2d_inverse_level(const dwt2d_plan* plan, const float* const in[4],
+                                       const size_t in_pitch[4], float* image, size_t pitch,
+                                       int width, int height, void* stream);
+
+/* --- multi-level (Mallat pyramid), device buffers --------
+ * Layout: after level l the top-left w x h LL region is replaced by
+ * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL
+ * bands: at least dwt2d_workspace_bytes() bytes, or NULL to let the library
+ * take it from the stream-ordered allocator. Width and height must be
+ * divisible by 2^levels. */
+DWT2D_B200_API size_t dwt2d_workspace_bytes(int width, int height, int levels);
+DWT2D_B200_API int dwt2d_forward_mallat(const dwt2d_plan* plan, const float* image, size_t pitch,
+                                        int width, int height, int levels, float* out,
+                                        size_t out_pitch, void* scratch, void* stream);
+DWT2D_B200_API int dwt2d_inverse_mallat(const dwt2d_plan* inverse_plan, const float* in,
+                                        size_t in_pitch, int width, int height, int levels,
+                                        float* image, size_t pitch, void* scratch, void* stream);
+
+/* --- host buffers (end-to-end: H2D + kernels + D2H inside the call) ------- */
+
+/* run<float> on host planes (the reference's own calling convention,
+ * executor.hpp:196-197): synchronous, returns when out[] is filled. */
+DWT2D_B200_API int dwt2d_run_planar_host(const dwt2d_plan* plan, const float* const in[4],
+                                         float* const out[4], int w2, int h2);
+/* Mallat pyramid of a host image into a host buffer (both W x H, dense). */
+DWT2D_B200_API int dwt2d_forward_mallat_host(const dwt2d_plan* plan, const float* image,
+                                             int width, int height, int levels, float* out);
+DWT2D_B200_API int dwt2d_inverse_mallat_host(const dwt2d_plan* inverse_plan, const float* in,
+                                             int width, int height, int levels, float* image);
+
+/* --- misc ------------------------------------------------------------------- */
+DWT2D_B200_API const char* dwt2d_last_error(void);
+DWT2D_B200_API const char* dwt2d_version(void);
+/* number of ahead-of-time compiled level programs and their keys */
+DWT2D_B200_API int dwt2d_registry_size(void);
+DWT2D_B200_API const char* dwt2d_registry_key(int i);
+/* count of level-kernel launches issued by this process (for bench/tests) */
+DWT2D_B200_API uint64_t dwt2d_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DWT2D_B200_H */

@@ -1,0 +1,125 @@
+// C++ mirror of the reference executor API, running on the B200 kernels.
+//
+// Drop-in for proj/include/dwt2d/executor.hpp:41-248: ExecPlan<T>,
+// compile<T>(scheme, extension, workers), run<T>(plan, image),
+// inverse_lifting<T>(wavelet, image, workers). Same names, argument meaning
+// and std::invalid_argument behaviour. Everything below goes through the
+// C ABI in dwt2d_b200.h: the scheme is lowered on the host
+// (lowering.hpp) and handed over as plain tables; the kernel that runs is
+// the ahead-of-time sm_100a kernel whose tables have the same fingerprint.
+//
+// Differences a caller can see:
+//  * T must be float — the GPU path computes in float32 (the north-star
+//    precision); ExecPlan<double> is rejected at compile time.
+//  * `workers` is validated (>= 1) and recorded but does not change the
+//    result or the launch; the reference's worker bit-identity holds
+//    trivially.
+//  * barrier_count reports the reference's logical count (one per scheme
+//    step) although the GPU fuses all steps of a level into one pass.
+#pragma once
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "dwt2d_b200.h"
+#include "dwt2d_b200/image.hpp"
+#include "dwt2d_b200/lowering.hpp"
+#include "dwt2d_b200/schemes.hpp"
+
+namespace dwt2d_b200 {
+
+namespace detail {
+inline void throw_status(int rc) {
+  if (rc == DWT2D_OK) return;
+  const std::string msg = dwt2d_last_error();
+  if (rc == DWT2D_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+struct PlanDeleter {
+  void operator()(dwt2d_plan* p) const { dwt2d_plan_destroy(p); }
+};
+}  // namespace detail
+
+template <typename T>
+struct ExecPlan {
+  static_assert(std::is_same_v<T, float>,
+                "dwt2d_b200 runs the transform in float32 on the GPU: use ExecPlan<float>");
+  std::shared_ptr<dwt2d_plan> handle;  // null for a scheme without steps
+  Extension extension = Extension::periodic;
+  int worker_count = 1;
+  long logical_steps = 0;
+  long barrier_count = 0;  // set by run(): one per scheme step
+};
+
+// compile<T>: executor.hpp:52-103
+template <typename T>
+ExecPlan<T> compile(const Scheme& s, Extension ext, int workers) {
+  if (workers < 1) throw std::invalid_argument("compile: worker count must be at least 1");
+  ExecPlan<T> plan;
+  plan.extension = ext;
+  plan.worker_count = workers;
+  plan.logical_steps = long(s.steps.size());
+  if (s.steps.empty()) return plan;
+  const StepProgram prog = lower(s, default_lowering(s));
+  std::vector<dwt2d_row> rows;
+  std::vector<dwt2d_tap> taps;
+  for (const KernelStep& st : prog.steps)
+    for (const KernelRow& r : st.rows) {
+      dwt2d_row row{};
+      row.identity = r.identity;
+      row.scale = r.scale;
+      row.tap_begin = int32_t(taps.size());
+      for (const KernelTap& k : r.taps) taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+      row.tap_end = int32_t(taps.size());
+      rows.push_back(row);
+    }
+  dwt2d_program t{};
+  t.nsteps = int32_t(prog.steps.size());
+  t.rows = rows.data();
+  t.ntaps = int32_t(taps.size());
+  t.taps = taps.data();
+  t.logical_steps = int32_t(prog.logical_steps);
+  t.extension = ext == Extension::periodic ? DWT2D_PERIODIC : DWT2D_SYMMETRIC;
+  t.forward = s.kind != SchemeKind::inverse_lifting;
+  dwt2d_plan* raw = nullptr;
+  detail::throw_status(dwt2d_plan_create_from_program(&t, &raw));
+  plan.handle.reset(raw, detail::PlanDeleter{});
+  return plan;
+}
+
+// run<T>: executor.hpp:196-238 (host images; H2D, one fused pass, D2H)
+template <typename T>
+PolyphaseImage<T> run(ExecPlan<T>& plan, const PolyphaseImage<T>& in) {
+  const int w2 = in.comp_width(), h2 = in.comp_height();
+  if (w2 <= 0 || h2 <= 0) throw std::invalid_argument("run: empty input");
+  for (const auto& c : in.comp)
+    if (c.width != w2 || c.height != h2) throw std::invalid_argument("run: component size mismatch");
+  if (in.extension != plan.extension) throw std::invalid_argument("run: extension mode mismatch");
+  plan.barrier_count = 0;
+  if (!plan.handle) return in;
+  PolyphaseImage<T> out;
+  out.extension = in.extension;
+  const float* src[4];
+  float* dst[4];
+  for (int j = 0; j < 4; ++j) {
+    out.comp[j] = ImagePlane<T>(w2, h2);
+    src[j] = in.comp[j].samples.data();
+    dst[j] = out.comp[j].samples.data();
+  }
+  detail::throw_status(dwt2d_run_planar_host(plan.handle.get(), src, dst, w2, h2));
+  plan.barrier_count = plan.logical_steps;
+  return out;
+}
+
+// inverse_lifting<T>: executor.hpp:242-248
+template <typename T>
+PolyphaseImage<T> inverse_lifting(const WaveletSpec& w, const PolyphaseImage<T>& p, int workers = 1) {
+  ExecPlan<T> plan = compile<T>(build_inverse_lifting(w), p.extension, workers);
+  return run(plan, p);
+}
+
+}  // namespace dwt2d_b200

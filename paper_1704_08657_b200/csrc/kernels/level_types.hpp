@@ -1,0 +1,58 @@
+// Plain C++ types shared by the host runtime (compiled with g++) and the
+// CUDA level kernels: launch arguments, tap tables, registry entries.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <vector>
+
+namespace dwt2d_b200 {
+namespace gpu {
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kOutLanes = 30;  // lanes 1..30 store, 0 and 31 are halo
+
+struct TapDesc {
+  int j;   // source component
+  int dm;  // component-grid column offset
+  int dn;  // component-grid row offset
+  float w;
+};
+
+struct RowDesc {
+  int ident;  // 1: output component = input component (no arithmetic)
+  int tb, te; // tap range [tb, te)
+  float scale;
+};
+
+// Arguments of one level launch. Pitches are in floats.
+struct LevelArgs {
+  const float* in[4];   // interleaved input: in[0] is the image (2*h2 rows)
+  long long in_pitch[4];
+  float* out[4];        // interleaved output: out[0] is the image
+  long long out_pitch[4];
+  int w2, h2;           // component grid size
+  int nstrips;          // ceil(w2 / (30 * CW))
+  int nchunks;          // ceil(h2 / chunk_rows)
+  int chunk_rows;
+  int vec;              // 1: vector fast path valid (w2 % CW == 0, 16 B aligned)
+};
+
+using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
+
+struct PlanEntry {
+  const char* key;
+  unsigned long long fingerprint;
+  int cw;                      // component columns per lane
+  int up, down, left, right;   // level reach on the component grid
+  long taps_per_quad;
+  LevelLaunch planar;          // 4 planes -> 4 planes   (run() API)
+  LevelLaunch from_image;      // interleaved -> 4 planes (forward levels)
+  LevelLaunch to_image;        // 4 planes -> interleaved (inverse levels)
+};
+
+const std::vector<PlanEntry>& plan_registry();
+const PlanEntry* find_plan(unsigned long long fingerprint);
+
+}  // namespace gpu
+}  // namespace dwt2d_b200

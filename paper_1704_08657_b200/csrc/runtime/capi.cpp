@@ -1,0 +1,577 @@
+// C-ABI implementation (include/dwt2d_b200.h): plan creation from the host
+// algebra, kernel selection by tap-table fingerprint, level launches and the
+// Mallat multi-level driver. No CPU fallback exists: a program without a
+// compiled kernel is rejected with DWT2D_EUNSUPPORTED.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dwt2d_b200.h"
+#include "dwt2d_b200/lowering.hpp"
+#include "dwt2d_b200/schemes.hpp"
+#include "../kernels/level_types.hpp"
+
+using namespace dwt2d_b200;
+
+struct dwt2d_plan {
+  std::string key;
+  std::uint64_t fingerprint = 0;
+  const gpu::PlanEntry* entry = nullptr;  // null => identity program (copy)
+  int extension = DWT2D_PERIODIC;
+  int forward = 1;
+  int logical_steps = 0;
+  int substeps = 0;
+  long long operations = -1;
+  long long taps_per_quad = 0;
+  int left = 0, right = 0, up = 0, down = 0;
+  std::string description;
+  std::vector<dwt2d_row> rows;
+  std::vector<dwt2d_tap> taps;
+};
+
+namespace {
+
+thread_local std::string g_error;
+std::atomic<std::uint64_t> g_launches{0};
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, std::string msg) { throw Fail{code, std::move(msg)}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? DWT2D_ENOMEM : DWT2D_ECUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return DWT2D_OK;
+  } catch (const Fail& e) {
+    g_error = e.msg;
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return DWT2D_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return DWT2D_ENOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return DWT2D_EINVAL;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      return v;
+    cudaGetLastError();
+    return 148;
+  }();
+  return n;
+}
+
+bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+// Rows per warp work item: enough items for ~4 waves of 16 warps per SM,
+// but long enough that the (up + down) warm-up rows stay a small overhead.
+int chunk_rows_for(const dwt2d_plan& p, int w2, int h2, int nstrips) {
+  if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
+    const int v = std::atoi(env);
+    if (v > 0) return v;
+  }
+  const long long target = 4ll * 16 * sm_count();
+  const long long per_strip = std::max<long long>(1, target / std::max(1, nstrips));
+  int chunk = int((h2 + per_strip - 1) / per_strip);
+  const int floor_rows = std::max(8, 4 * (p.up + p.down));
+  chunk = std::max(chunk, std::min(floor_rows, h2));
+  chunk = std::min(chunk, 512);
+  return std::max(1, chunk);
+}
+
+enum Layout { kPlanar, kFromImage, kToImage };
+
+void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
+  if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+  const gpu::PlanEntry& e = *p.entry;
+  const int cw = e.cw;
+  a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
+  a.chunk_rows = chunk_rows_for(p, a.w2, a.h2, a.nstrips);
+  a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
+  bool vec = a.w2 % cw == 0;
+  const bool in_il = layout == kFromImage, out_il = layout == kToImage;
+  for (int j = 0; j < 4; ++j) {
+    if (!in_il || j == 0) {
+      const size_t al = in_il ? 16 : size_t(4 * cw);
+      vec = vec && aligned(a.in[j], al) && (a.in_pitch[j] * 4) % al == 0;
+    }
+    if (!out_il || j == 0) {
+      const size_t al = out_il ? 16 : size_t(4 * cw);
+      vec = vec && aligned(a.out[j], al) && (a.out_pitch[j] * 4) % al == 0;
+    }
+  }
+  a.vec = vec ? 1 : 0;
+  gpu::LevelLaunch fn = layout == kPlanar ? e.planar : layout == kFromImage ? e.from_image : e.to_image;
+  if (!fn)
+    fail(DWT2D_EINVAL, layout == kToImage ? "inverse_level: plan is not an inverse plan"
+                                          : "forward_level: plan is an inverse plan");
+  cuda_check(fn(a, st), "level kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void require_plan(const dwt2d_plan* p) {
+  if (!p) fail(DWT2D_EINVAL, "null plan");
+}
+
+void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
+  p.key = prog.key;
+  p.fingerprint = prog.fingerprint();
+  p.logical_steps = int(prog.logical_steps);
+  p.substeps = int(prog.steps.size());
+  p.taps_per_quad = prog.taps_per_quad();
+  p.left = prog.left, p.right = prog.right, p.up = prog.up, p.down = prog.down;
+  p.extension = extension;
+  p.rows.clear(), p.taps.clear();
+  for (const KernelStep& st : prog.steps)
+    for (const KernelRow& r : st.rows) {
+      dwt2d_row row{};
+      row.identity = r.identity;
+      row.scale = r.scale;
+      row.tap_begin = int32_t(p.taps.size());
+      for (const KernelTap& k : r.taps) p.taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+      row.tap_end = int32_t(p.taps.size());
+      p.rows.push_back(row);
+    }
+  bool identity = true;
+  for (const KernelStep& st : prog.steps)
+    for (const KernelRow& r : st.rows) identity = identity && r.identity;
+  if (identity) return;  // pure copy, no kernel (pairless wavelet)
+  if (extension != DWT2D_PERIODIC)
+    fail(DWT2D_EUNSUPPORTED, "symmetric extension has no compiled kernel yet (" + p.key + ")");
+  p.entry = gpu::find_plan(p.fingerprint);
+  if (!p.entry)
+    fail(DWT2D_EUNSUPPORTED, "no compiled level kernel for program " + p.key +
+                                 " (custom wavelets are not compiled ahead of time)");
+}
+
+StepProgram program_from_tables(const dwt2d_program& t) {
+  if (t.nsteps < 0 || t.ntaps < 0 || (t.nsteps && !t.rows) || (t.ntaps && !t.taps))
+    fail(DWT2D_EINVAL, "malformed program tables");
+  StepProgram p;
+  p.key = "program";
+  p.logical_steps = t.logical_steps;
+  for (int s = 0; s < t.nsteps; ++s) {
+    KernelStep st;
+    for (int r = 0; r < 4; ++r) {
+      const dwt2d_row& row = t.rows[s * 4 + r];
+      KernelRow& kr = st.rows[r];
+      kr.identity = row.identity != 0;
+      kr.scale = row.scale;
+      if (row.tap_begin < 0 || row.tap_end > t.ntaps || row.tap_begin > row.tap_end)
+        fail(DWT2D_EINVAL, "malformed program tap range");
+      for (int i = row.tap_begin; i < row.tap_end; ++i) {
+        const dwt2d_tap& tp = t.taps[i];
+        if (tp.comp < 0 || tp.comp > 3) fail(DWT2D_EINVAL, "malformed program tap component");
+        KernelTap k;
+        k.comp = tp.comp, k.dm = tp.dm, k.dn = tp.dn, k.w = tp.w, k.coef = tp.w;
+        kr.taps.push_back(k);
+        st.min_dm = std::min(st.min_dm, k.dm), st.max_dm = std::max(st.max_dm, k.dm);
+        st.min_dn = std::min(st.min_dn, k.dn), st.max_dn = std::max(st.max_dn, k.dn);
+      }
+    }
+    p.steps.push_back(st);
+  }
+  for (const KernelStep& st : p.steps) {
+    p.left -= st.min_dm, p.right += st.max_dm, p.up -= st.min_dn, p.down += st.max_dn;
+  }
+  return p;
+}
+
+void copy_planes(const float* const in[4], const size_t in_pitch[4], float* const out[4],
+                 const size_t out_pitch[4], int w2, int h2, cudaStream_t st) {
+  for (int j = 0; j < 4; ++j)
+    cuda_check(cudaMemcpy2DAsync(out[j], out_pitch[j] * 4, in[j], in_pitch[j] * 4, size_t(w2) * 4, h2,
+                                 cudaMemcpyDeviceToDevice, st),
+               "copy");
+}
+
+void check_pyramid(int W, int H, int levels) {
+  if (W <= 0 || H <= 0) fail(DWT2D_EINVAL, "pyramid: empty image");
+  if (levels < 1) fail(DWT2D_EINVAL, "pyramid: levels must be at least 1");
+  if (levels > 30 || (W % (1 << levels)) || (H % (1 << levels)))
+    fail(DWT2D_EINVAL, "pyramid: width and height must be divisible by 2^levels");
+}
+
+// intermediate LL band of level k (k >= 1) in the workspace: odd k at A, even at B
+float* ll_slot(float* ws, int W, int H, int k) {
+  const size_t a = size_t(W / 2) * size_t(H / 2);
+  return (k & 1) ? ws : ws + ((a + 63) & ~size_t(63));
+}
+
+struct Workspace {
+  float* ptr = nullptr;
+  bool owned = false;
+  cudaStream_t st = nullptr;
+  ~Workspace() {
+    if (owned && ptr) cudaFreeAsync(ptr, st);
+  }
+};
+
+void get_workspace(Workspace& w, void* scratch, int W, int H, int levels, cudaStream_t st) {
+  const size_t bytes = dwt2d_workspace_bytes(W, H, levels);
+  w.st = st;
+  if (scratch || bytes == 0) {
+    w.ptr = static_cast<float*>(scratch);
+    return;
+  }
+  void* p = nullptr;
+  cuda_check(cudaMallocAsync(&p, bytes, st), "workspace allocation");
+  w.ptr = static_cast<float*>(p);
+  w.owned = true;
+}
+
+void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W, int H, int levels,
+                    float* out, size_t out_pitch, float* ws, cudaStream_t st) {
+  const float* cur = image;
+  size_t cur_pitch = pitch;
+  for (int l = 1; l <= levels; ++l) {
+    const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
+    gpu::LevelArgs a{};
+    a.in[0] = a.in[1] = a.in[2] = a.in[3] = cur;
+    for (int j = 0; j < 4; ++j) a.in_pitch[j] = (long long)cur_pitch;
+    float* ll = l == levels ? out : ll_slot(ws, W, H, l);
+    const size_t ll_pitch = l == levels ? out_pitch : size_t(w2);
+    a.out[0] = ll;
+    a.out_pitch[0] = (long long)ll_pitch;
+    a.out[1] = out + w2;
+    a.out[2] = out + size_t(h2) * out_pitch;
+    a.out[3] = out + size_t(h2) * out_pitch + w2;
+    a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = (long long)out_pitch;
+    a.w2 = w2, a.h2 = h2;
+    launch(p, a, kFromImage, st);
+    cur = ll;
+    cur_pitch = ll_pitch;
+  }
+}
+
+void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W, int H, int levels,
+                    float* image, size_t pitch, float* ws, cudaStream_t st) {
+  const float* ll = in;
+  size_t ll_pitch = in_pitch;
+  for (int l = levels; l >= 1; --l) {
+    const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
+    gpu::LevelArgs a{};
+    a.in[0] = ll;
+    a.in_pitch[0] = (long long)ll_pitch;
+    a.in[1] = in + w2;
+    a.in[2] = in + size_t(h2) * in_pitch;
+    a.in[3] = in + size_t(h2) * in_pitch + w2;
+    a.in_pitch[1] = a.in_pitch[2] = a.in_pitch[3] = (long long)in_pitch;
+    float* dst = l == 1 ? image : ll_slot(ws, W, H, l - 1);
+    const size_t dst_pitch = l == 1 ? pitch : size_t(w);
+    a.out[0] = a.out[1] = a.out[2] = a.out[3] = dst;
+    for (int j = 0; j < 4; ++j) a.out_pitch[j] = (long long)dst_pitch;
+    a.w2 = w2, a.h2 = h2;
+    if (!p.entry) fail(DWT2D_EUNSUPPORTED, "identity inverse pyramid");
+    launch(p, a, kToImage, st);
+    ll = dst;
+    ll_pitch = dst_pitch;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" {
+
+const char* dwt2d_last_error(void) { return g_error.c_str(); }
+const char* dwt2d_version(void) { return "dwt2d_b200 0.1 (sm_100a)"; }
+uint64_t dwt2d_launch_count(void) { return g_launches.load(); }
+
+int dwt2d_registry_size(void) { return int(gpu::plan_registry().size()); }
+const char* dwt2d_registry_key(int i) {
+  const auto& r = gpu::plan_registry();
+  return (i >= 0 && i < int(r.size())) ? r[i].key : nullptr;
+}
+
+int dwt2d_plan_create(const dwt2d_plan_desc* d, dwt2d_plan** out) {
+  return guard([&] {
+    if (!d || !out || !d->wavelet) fail(DWT2D_EINVAL, "null argument");
+    *out = nullptr;
+    if (d->workers < 1) fail(DWT2D_EINVAL, "compile: worker count must be at least 1");
+    if (d->scheme < 0 || d->scheme > DWT2D_INVERSE_LIFTING) fail(DWT2D_EINVAL, "unknown scheme");
+    if (d->extension != DWT2D_PERIODIC && d->extension != DWT2D_SYMMETRIC)
+      fail(DWT2D_EINVAL, "unknown extension");
+    const WaveletSpec w = resolve_wavelet(d->wavelet);
+    Scheme s;
+    if (d->scheme == DWT2D_INVERSE_LIFTING) {
+      if (d->optimized) fail(DWT2D_EINVAL, "optimize_constant_split: inverse schemes are not optimizable");
+      s = build_inverse_lifting(w);
+    } else {
+      s = build_scheme(static_cast<SchemeKind>(d->scheme), w);
+      if (d->optimized) s = optimize_constant_split(s, w);
+    }
+    Lowering mode = default_lowering(s);
+    if (d->lowering == DWT2D_LOWERING_COMPOSED) mode = Lowering::composed;
+    if (d->lowering == DWT2D_LOWERING_FACTORED) mode = Lowering::factored;
+    const StepProgram prog = lower(s, mode);
+    auto p = std::make_unique<dwt2d_plan>();
+    p->forward = d->scheme != DWT2D_INVERSE_LIFTING;
+    p->operations = count_operations(s);
+    p->description = describe(s);
+    finalize_plan(*p, prog, d->extension);
+    *out = p.release();
+  });
+}
+
+int dwt2d_plan_create_from_program(const dwt2d_program* t, dwt2d_plan** out) {
+  return guard([&] {
+    if (!t || !out) fail(DWT2D_EINVAL, "null argument");
+    *out = nullptr;
+    const StepProgram prog = program_from_tables(*t);
+    auto p = std::make_unique<dwt2d_plan>();
+    p->forward = t->forward != 0;
+    finalize_plan(*p, prog, t->extension);
+    if (p->entry) p->key = p->entry->key;
+    *out = p.release();
+  });
+}
+
+void dwt2d_plan_destroy(dwt2d_plan* p) { delete p; }
+
+int dwt2d_plan_get_info(const dwt2d_plan* p, dwt2d_plan_info* info) {
+  return guard([&] {
+    require_plan(p);
+    if (!info) fail(DWT2D_EINVAL, "null info");
+    std::memset(info, 0, sizeof *info);
+    std::snprintf(info->key, sizeof info->key, "%s", p->key.c_str());
+    info->fingerprint = p->fingerprint;
+    info->logical_steps = p->logical_steps;
+    info->substeps = p->substeps;
+    info->operations = p->operations;
+    info->taps_per_quad = p->taps_per_quad;
+    info->reach_left = p->left, info->reach_right = p->right;
+    info->reach_up = p->up, info->reach_down = p->down;
+    info->columns_per_lane = p->entry ? p->entry->cw : 0;
+    info->forward = p->forward;
+    info->extension = p->extension;
+  });
+}
+
+int dwt2d_plan_get_tables(const dwt2d_plan* p, dwt2d_row* rows, int32_t rows_cap, dwt2d_tap* taps,
+                          int32_t taps_cap, int32_t* nrows, int32_t* ntaps) {
+  return guard([&] {
+    require_plan(p);
+    if (nrows) *nrows = int32_t(p->rows.size());
+    if (ntaps) *ntaps = int32_t(p->taps.size());
+    if (rows) {
+      if (rows_cap < int32_t(p->rows.size())) fail(DWT2D_EINVAL, "rows buffer too small");
+      std::copy(p->rows.begin(), p->rows.end(), rows);
+    }
+    if (taps) {
+      if (taps_cap < int32_t(p->taps.size())) fail(DWT2D_EINVAL, "taps buffer too small");
+      std::copy(p->taps.begin(), p->taps.end(), taps);
+    }
+  });
+}
+
+int dwt2d_plan_describe(const dwt2d_plan* p, char* buf, size_t len) {
+  return guard([&] {
+    require_plan(p);
+    if (!buf || len < p->description.size() + 1) fail(DWT2D_EINVAL, "describe: buffer too small");
+    std::memcpy(buf, p->description.c_str(), p->description.size() + 1);
+  });
+}
+
+int dwt2d_run_planar(const dwt2d_plan* p, const float* const in[4], const size_t in_pitch[4],
+                     float* const out[4], const size_t out_pitch[4], int w2, int h2, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!in || !out || !in_pitch || !out_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    if (!p->entry) return copy_planes(in, in_pitch, out, out_pitch, w2, h2, as_stream(stream));
+    gpu::LevelArgs a{};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = in[j], a.out[j] = out[j];
+      a.in_pitch[j] = (long long)in_pitch[j], a.out_pitch[j] = (long long)out_pitch[j];
+      if (in_pitch[j] < size_t(w2) || out_pitch[j] < size_t(w2)) fail(DWT2D_EINVAL, "pitch < width");
+    }
+    a.w2 = w2, a.h2 = h2;
+    launch(*p, a, kPlanar, as_stream(stream));
+  });
+}
+
+int dwt2d_forward_level(const dwt2d_plan* p, const float* image, size_t pitch, int width, int height,
+                        float* const out[4], const size_t out_pitch[4], void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out || !out_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (width <= 0 || height <= 0) fail(DWT2D_EINVAL, "polyphase_split: empty image");
+    if (width % 2) fail(DWT2D_EINVAL, "polyphase_split: odd image width");
+    if (height % 2) fail(DWT2D_EINVAL, "polyphase_split: odd image height");
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    gpu::LevelArgs a{};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = image, a.in_pitch[j] = (long long)pitch;
+      a.out[j] = out[j], a.out_pitch[j] = (long long)out_pitch[j];
+    }
+    a.w2 = width / 2, a.h2 = height / 2;
+    launch(*p, a, kFromImage, as_stream(stream));
+  });
+}
+
+int dwt2d_inverse_level(const dwt2d_plan* p, const float* const in[4], const size_t in_pitch[4],
+                        float* image, size_t pitch, int width, int height, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !in || !in_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (width <= 0 || height <= 0 || width % 2 || height % 2)
+      fail(DWT2D_EINVAL, "inverse_level: image sides must be positive and even");
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    gpu::LevelArgs a{};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = in[j], a.in_pitch[j] = (long long)in_pitch[j];
+      a.out[j] = image, a.out_pitch[j] = (long long)pitch;
+    }
+    a.w2 = width / 2, a.h2 = height / 2;
+    launch(*p, a, kToImage, as_stream(stream));
+  });
+}
+
+size_t dwt2d_workspace_bytes(int width, int height, int levels) {
+  if (levels < 2 || width <= 0 || height <= 0) return 0;
+  const size_t a = size_t(width / 2) * size_t(height / 2);
+  const size_t b = levels >= 3 ? size_t(width / 4) * size_t(height / 4) : 0;
+  return (((a + 63) & ~size_t(63)) + b) * sizeof(float);
+}
+
+int dwt2d_forward_mallat(const dwt2d_plan* p, const float* image, size_t pitch, int W, int H, int levels,
+                         float* out, size_t out_pitch, void* scratch, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
+    check_pyramid(W, H, levels);
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    Workspace ws;
+    get_workspace(ws, scratch, W, H, levels, as_stream(stream));
+    forward_mallat(*p, image, pitch, W, H, levels, out, out_pitch, ws.ptr, as_stream(stream));
+  });
+}
+
+int dwt2d_inverse_mallat(const dwt2d_plan* p, const float* in, size_t in_pitch, int W, int H, int levels,
+                         float* image, size_t pitch, void* scratch, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !in) fail(DWT2D_EINVAL, "null argument");
+    if (p->forward) fail(DWT2D_EINVAL, "inverse_mallat: plan is not an inverse plan");
+    check_pyramid(W, H, levels);
+    Workspace ws;
+    get_workspace(ws, scratch, W, H, levels, as_stream(stream));
+    inverse_mallat(*p, in, in_pitch, W, H, levels, image, pitch, ws.ptr, as_stream(stream));
+  });
+}
+
+int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* const out[4], int w2, int h2) {
+  return guard([&] {
+    require_plan(p);
+    if (!in || !out) fail(DWT2D_EINVAL, "null argument");
+    if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    const size_t n = size_t(w2) * h2;
+    float* dev = nullptr;
+    cuda_check(cudaMalloc(&dev, 8 * n * sizeof(float)), "device allocation");
+    std::unique_ptr<float, decltype(&cudaFree)> hold(dev, &cudaFree);
+    const float* din[4];
+    float* dout[4];
+    size_t pitch[4];
+    for (int j = 0; j < 4; ++j) {
+      din[j] = dev + j * n;
+      dout[j] = dev + (4 + j) * n;
+      pitch[j] = size_t(w2);
+      cuda_check(cudaMemcpy(dev + j * n, in[j], n * 4, cudaMemcpyHostToDevice), "H2D");
+    }
+    if (!p->entry) {
+      copy_planes(din, pitch, dout, pitch, w2, h2, nullptr);
+    } else {
+      gpu::LevelArgs a{};
+      for (int j = 0; j < 4; ++j) {
+        a.in[j] = din[j], a.out[j] = dout[j];
+        a.in_pitch[j] = a.out_pitch[j] = w2;
+      }
+      a.w2 = w2, a.h2 = h2;
+      launch(*p, a, kPlanar, nullptr);
+    }
+    for (int j = 0; j < 4; ++j)
+      cuda_check(cudaMemcpy(out[j], dout[j], n * 4, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, int H, int levels, float* out) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
+    check_pyramid(W, H, levels);
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    const size_t n = size_t(W) * H;
+    cudaStream_t st = nullptr;
+    void* d_img = nullptr;
+    void* d_out = nullptr;
+    cuda_check(cudaMallocAsync(&d_img, n * 4, st), "device allocation");
+    cuda_check(cudaMallocAsync(&d_out, n * 4, st), "device allocation");
+    Workspace ws;
+    get_workspace(ws, nullptr, W, H, levels, st);
+    cuda_check(cudaMemcpyAsync(d_img, image, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+    forward_mallat(*p, static_cast<float*>(d_img), W, W, H, levels, static_cast<float*>(d_out), W, ws.ptr, st);
+    cuda_check(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cudaFreeAsync(d_img, st);
+    cudaFreeAsync(d_out, st);
+    cuda_check(cudaStreamSynchronize(st), "synchronize");
+  });
+}
+
+int dwt2d_inverse_mallat_host(const dwt2d_plan* p, const float* in, int W, int H, int levels, float* image) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !in) fail(DWT2D_EINVAL, "null argument");
+    if (p->forward) fail(DWT2D_EINVAL, "inverse_mallat: plan is not an inverse plan");
+    check_pyramid(W, H, levels);
+    const size_t n = size_t(W) * H;
+    cudaStream_t st = nullptr;
+    void* d_in = nullptr;
+    void* d_img = nullptr;
+    cuda_check(cudaMallocAsync(&d_in, n * 4, st), "device allocation");
+    cuda_check(cudaMallocAsync(&d_img, n * 4, st), "device allocation");
+    Workspace ws;
+    get_workspace(ws, nullptr, W, H, levels, st);
+    cuda_check(cudaMemcpyAsync(d_in, in, n * 4, cudaMemcpyHostToDevice, st), "H2D");
+    inverse_mallat(*p, static_cast<float*>(d_in), W, W, H, levels, static_cast<float*>(d_img), W, ws.ptr, st);
+    cuda_check(cudaMemcpyAsync(image, d_img, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cudaFreeAsync(d_in, st);
+    cudaFreeAsync(d_img, st);
+    cuda_check(cudaStreamSynchronize(st), "synchronize");
+  });
+}
+
+}  // extern "C"

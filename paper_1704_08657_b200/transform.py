@@ -1,0 +1,188 @@
+"""Python face of the C ABI: plans and transforms on torch CUDA tensors or
+host numpy arrays. Mirrors the reference's call sequence
+build_scheme -> optimize_constant_split -> compile -> run
+(proj/src/bench.cpp:33-39, executor.hpp:52-238) with a GPU plan.
+
+Device tensors are float32 CUDA tensors with unit stride along rows; their
+row stride is passed as the pitch. Work is enqueued on the current torch
+stream unless a stream is given.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from . import native as N
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev(t, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise TypeError(f"{name} must be a float32 CUDA tensor")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    return t.data_ptr(), t.stride(0)
+
+
+class Plan:
+    """A compiled transform plan (forward scheme or inverse lifting)."""
+
+    def __init__(self, wavelet: str = "cdf97", scheme: str = "nonseparable-lifting",
+                 optimized: bool = False, extension: str = "periodic",
+                 lowering: str = "default", workers: int = 1):
+        if scheme not in N.SCHEMES:
+            raise ValueError(f"unknown scheme: {scheme} (valid: {' '.join(N.SCHEMES)})")
+        desc = N.PlanDesc(wavelet.encode(), N.SCHEMES[scheme], int(optimized),
+                          N.EXTENSIONS[extension], N.LOWERINGS[lowering], int(workers))
+        h = ctypes.c_void_p()
+        N.check(N.lib.dwt2d_plan_create(ctypes.byref(desc), ctypes.byref(h)))
+        self._h = h
+        self.wavelet, self.scheme, self.optimized = wavelet, scheme, bool(optimized)
+        self.extension = extension
+
+    @classmethod
+    def from_program(cls, rows, taps, *, logical_steps: int, forward: bool = True,
+                     extension: str = "periodic") -> "Plan":
+        """compile<float> of explicit tables: rows = [(identity, tb, te, scale)]*4*nsteps,
+        taps = [(comp, dm, dn, w)]."""
+        R = (N.Row * max(1, len(rows)))(*[N.Row(*r) for r in rows])
+        T = (N.Tap * max(1, len(taps)))(*[N.Tap(*t) for t in taps])
+        prog = N.Program(len(rows) // 4, R, len(taps), T, logical_steps, N.EXTENSIONS[extension],
+                         int(forward))
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        N.check(N.lib.dwt2d_plan_create_from_program(ctypes.byref(prog), ctypes.byref(h)))
+        self._h = h
+        self.wavelet, self.scheme, self.optimized, self.extension = "program", "program", False, extension
+        return self
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            N.lib.dwt2d_plan_destroy(h)
+            self._h = None
+
+    # -- introspection -------------------------------------------------
+    @property
+    def info(self) -> dict:
+        i = N.PlanInfo()
+        N.check(N.lib.dwt2d_plan_get_info(self._h, ctypes.byref(i)))
+        return {f: (getattr(i, f).decode() if f == "key" else getattr(i, f)) for f, _ in N.PlanInfo._fields_}
+
+    def tables(self):
+        """(rows, taps) the level kernel executes: rows = [(identity, tb, te, scale)],
+        taps = [(comp, dm, dn, w)] (weights as float32 values)."""
+        nr, nt = ctypes.c_int32(), ctypes.c_int32()
+        N.check(N.lib.dwt2d_plan_get_tables(self._h, None, 0, None, 0, ctypes.byref(nr), ctypes.byref(nt)))
+        R = (N.Row * max(1, nr.value))()
+        T = (N.Tap * max(1, nt.value))()
+        N.check(N.lib.dwt2d_plan_get_tables(self._h, R, nr.value, T, nt.value, ctypes.byref(nr),
+                                            ctypes.byref(nt)))
+        rows = [(bool(r.identity), r.tap_begin, r.tap_end, r.scale) for r in R[: nr.value]]
+        taps = [(t.comp, t.dm, t.dn, t.w) for t in T[: nt.value]]
+        return rows, taps
+
+    def describe(self) -> str:
+        buf = ctypes.create_string_buffer(1 << 18)
+        N.check(N.lib.dwt2d_plan_describe(self._h, buf, len(buf)))
+        return buf.value.decode()
+
+    # -- device tensors ------------------------------------------------
+    def run(self, planes: Sequence, out: Sequence | None = None, stream=None):
+        """run<float> on four [h2, w2] CUDA tensors (ee, oe, eo, oo)."""
+        import torch
+        h2, w2 = planes[0].shape
+        if out is None:
+            out = [torch.empty((h2, w2), dtype=torch.float32, device=planes[0].device) for _ in range(4)]
+        ip, op = zip(*[_dev(p, "plane") for p in planes]), zip(*[_dev(o, "out") for o in out])
+        iptr, ipit = list(ip)
+        optr, opit = list(op)
+        N.check(N.lib.dwt2d_run_planar(self._h, N._P4(*iptr), N._S4(*ipit), N._P4(*optr), N._S4(*opit),
+                                       w2, h2, _stream_handle(stream)))
+        return list(out)
+
+    def forward_level(self, image, out: Sequence | None = None, stream=None):
+        import torch
+        H, W = image.shape
+        if out is None:
+            out = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=image.device) for _ in range(4)]
+        ptr, pitch = _dev(image, "image")
+        optr, opit = zip(*[_dev(o, "out") for o in out])
+        N.check(N.lib.dwt2d_forward_level(self._h, ptr, pitch, W, H, N._P4(*optr), N._S4(*opit),
+                                          _stream_handle(stream)))
+        return list(out)
+
+    def inverse_level(self, planes: Sequence, image=None, stream=None):
+        import torch
+        h2, w2 = planes[0].shape
+        if image is None:
+            image = torch.empty((2 * h2, 2 * w2), dtype=torch.float32, device=planes[0].device)
+        iptr, ipit = zip(*[_dev(p, "plane") for p in planes])
+        ptr, pitch = _dev(image, "image")
+        N.check(N.lib.dwt2d_inverse_level(self._h, N._P4(*iptr), N._S4(*ipit), ptr, pitch, 2 * w2, 2 * h2,
+                                          _stream_handle(stream)))
+        return image
+
+    def forward_mallat(self, image, levels: int, out=None, scratch=None, stream=None):
+        import torch
+        H, W = image.shape
+        if out is None:
+            out = torch.empty((H, W), dtype=torch.float32, device=image.device)
+        ptr, pitch = _dev(image, "image")
+        optr, opitch = _dev(out, "out")
+        N.check(N.lib.dwt2d_forward_mallat(self._h, ptr, pitch, W, H, levels, optr, opitch,
+                                           None if scratch is None else scratch.data_ptr(),
+                                           _stream_handle(stream)))
+        return out
+
+    def inverse_mallat(self, coeffs, levels: int, image=None, scratch=None, stream=None):
+        import torch
+        H, W = coeffs.shape
+        if image is None:
+            image = torch.empty((H, W), dtype=torch.float32, device=coeffs.device)
+        cptr, cpitch = _dev(coeffs, "coeffs")
+        ptr, pitch = _dev(image, "image")
+        N.check(N.lib.dwt2d_inverse_mallat(self._h, cptr, cpitch, W, H, levels, ptr, pitch,
+                                           None if scratch is None else scratch.data_ptr(),
+                                           _stream_handle(stream)))
+        return image
+
+    # -- host arrays (H2D + kernels + D2H inside the call) -------------
+    def run_host(self, planes: Sequence[np.ndarray]) -> list[np.ndarray]:
+        planes = [np.ascontiguousarray(p, dtype=np.float32) for p in planes]
+        h2, w2 = planes[0].shape
+        out = [np.empty_like(planes[0]) for _ in range(4)]
+        N.check(N.lib.dwt2d_run_planar_host(self._h, N._P4(*[p.ctypes.data for p in planes]),
+                                            N._P4(*[o.ctypes.data for o in out]), w2, h2))
+        return out
+
+    def forward_mallat_host(self, image: np.ndarray, levels: int, out: np.ndarray | None = None):
+        image = np.ascontiguousarray(image, dtype=np.float32)
+        H, W = image.shape
+        if out is None:
+            out = np.empty_like(image)
+        N.check(N.lib.dwt2d_forward_mallat_host(self._h, image.ctypes.data, W, H, levels, out.ctypes.data))
+        return out
+
+    def inverse_mallat_host(self, coeffs: np.ndarray, levels: int, out: np.ndarray | None = None):
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float32)
+        H, W = coeffs.shape
+        if out is None:
+            out = np.empty_like(coeffs)
+        N.check(N.lib.dwt2d_inverse_mallat_host(self._h, coeffs.ctypes.data, W, H, levels, out.ctypes.data))
+        return out
+
+
+def workspace_bytes(width: int, height: int, levels: int) -> int:
+    return int(N.lib.dwt2d_workspace_bytes(width, height, levels))
