@@ -241,23 +241,25 @@ def main():
     assert torch.equal(ref_out, out), "per-level driver and forward_mallat disagree"
 
     # capture K steps with per-level events into one graph
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(LEVELS + 1)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(LEVELS + 1)]
+           for _ in range(args.steps)]
     graph = torch.cuda.CUDAGraph()
     launches0 = dwt.launch_count()
     with torch.cuda.graph(graph, stream=stream):
         for k in range(args.steps):
             step(evs[k])
     launches_captured = dwt.launch_count() - launches0
-    graph.replay()  # untimed replay warms the graph
+    with torch.cuda.stream(stream):
+        graph.replay()  # untimed replay warms the graph
     torch.cuda.synchronize()
 
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if n > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         t0.record(stream)
-        graph.replay()
+        graph.replay()  # replays on the current stream (= `stream` here)
         t1.record(stream)
         t1.synchronize()
         if n > 1:

@@ -90,6 +90,7 @@ typedef struct {
   int32_t logical_steps;   /* count_steps(scheme): the reference's barrier count */
   int32_t extension;       /* dwt2d_extension */
   int32_t forward;         /* 1 forward analysis, 0 inverse synthesis */
+  int32_t fused_multiply_add; /* 0: round(w*v) then add (reference arithmetic), 1: fma per tap */
 } dwt2d_program;
 
 typedef struct dwt2d_plan dwt2d_plan;
@@ -105,6 +106,7 @@ typedef struct {
   int32_t columns_per_lane; /* CW of the level kernel */
   int32_t forward;
   int32_t extension;
+  int32_t fused_multiply_add;
 } dwt2d_plan_info;
 
 /* --- plans -------------------------------------------------------------- */

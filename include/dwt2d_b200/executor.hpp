@@ -85,6 +85,7 @@ ExecPlan<T> compile(const Scheme& s, Extension ext, int workers) {
   t.logical_steps = int32_t(prog.logical_steps);
   t.extension = ext == Extension::periodic ? DWT2D_PERIODIC : DWT2D_SYMMETRIC;
   t.forward = s.kind != SchemeKind::inverse_lifting;
+  t.fused_multiply_add = prog.fused_multiply_add;
   dwt2d_plan* raw = nullptr;
   detail::throw_status(dwt2d_plan_create_from_program(&t, &raw));
   plan.handle.reset(raw, detail::PlanDeleter{});

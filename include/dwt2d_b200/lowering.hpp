@@ -8,9 +8,10 @@
 // "barriers" become register/shuffle dependencies. Two lowerings:
 //
 //   composed  one sub-step per fused group, the composed matrix with the
-//             reference's tap order (source component, then (dn, dm)) and
-//             its float weights (T)(coef * pre) — reproduces the reference's
-//             per-sample arithmetic exactly (executor.hpp:85-97, :179-184).
+//             reference's tap order (source component, then (dn, dm)), its
+//             float weights (T)(coef * pre) and its rounding (a multiply and
+//             an add per tap) — reproduces the reference's float32 executor
+//             bit for bit (executor.hpp:85-97, :179-184).
 //   factored  one sub-step per factor (rightmost first), so the optimized
 //             schemes really execute the paper's reduced operation count
 //             (scheme.cpp:279-378 builds the factors; the reference composes
@@ -52,6 +53,10 @@ struct StepProgram {
   std::string key;  // "<wavelet>/<scheme-id>/<base|opt>/<composed|factored>"
   std::vector<KernelStep> steps;
   long logical_steps = 0;  // count_steps(scheme): the reference's barrier count
+  // rounding model of every tap: false = round(w*v) then round(acc + p), the
+  // reference executor's arithmetic (bit-exact to its float32 path); true =
+  // one fused multiply-add per tap (factored lowering)
+  bool fused_multiply_add = false;
   // accumulated reach of the whole level: output (x, y) depends on input
   // columns x-left..x+right and rows y-up..y+down
   int left = 0, right = 0, up = 0, down = 0;

@@ -68,6 +68,7 @@ StepProgram lower(const Scheme& s, Lowering mode) {
   p.key = s.wavelet + "/" + scheme_id(s.kind) + "/" + (s.optimized ? "opt" : "base") + "/" +
           (mode == Lowering::composed ? "composed" : "factored");
   p.logical_steps = long(s.steps.size());
+  p.fused_multiply_add = mode == Lowering::factored;
   // flatten to the matrices actually executed, in execution order
   std::vector<PolyMatrix> mats;
   for (const FusedGroup& g : s.steps) {
@@ -108,6 +109,7 @@ std::uint64_t StepProgram::fingerprint() const {
     }
   };
   mix(steps.size());
+  mix(fused_multiply_add ? 1 : 0);
   for (const KernelStep& st : steps)
     for (const KernelRow& r : st.rows) {
       std::uint32_t sb;

@@ -127,9 +127,10 @@ __device__ __forceinline__ void eval_step(const float (&in)[D][4][CW], float (&o
     } else if constexpr (row.tb == row.te) {  // an all-zero matrix row
       sfor<0, CW>([&](auto C_) { out[r][decltype(C_)::value] = 0.0f; });
     } else {
-      // acc = 0 + w0*v0 + w1*v1 + ... in table order, one rounding per tap
-      // (the reference's `acc += f.w * src` with FMA contraction); the first
-      // tap is a plain product (a copy when w0 == 1).
+      // acc = 0 + w0*v0 + w1*v1 + ... in table order. Composed programs round
+      // like the reference's `acc += f.w * src` (executor.hpp:183: product
+      // rounded, then the sum); factored programs fuse each tap into one
+      // fma. The first tap is a plain product (a copy when w0 == 1).
       float acc[CW];
       constexpr int tb = row.tb;
       constexpr float sc = row.scale;
@@ -143,8 +144,10 @@ __device__ __forceinline__ void eval_step(const float (&in)[D][4][CW], float (&o
         sfor<0, CW>([&](auto C_) {
           constexpr int c = decltype(C_)::value;
           const float v = fetch<c + dm, CW>(in[k][j]);
-          if constexpr (!first)
+          if constexpr (!first && P::kFma)
             acc[c] = __fmaf_rn(w, v, acc[c]);
+          else if constexpr (!first)  // reference rounding: product, then sum
+            acc[c] = __fadd_rn(acc[c], w == 1.0f ? v : __fmul_rn(w, v));
           else if constexpr (w == 1.0f)
             acc[c] = v;
           else

@@ -32,6 +32,7 @@ struct dwt2d_plan {
   long long operations = -1;
   long long taps_per_quad = 0;
   int left = 0, right = 0, up = 0, down = 0;
+  int fma = 0;
   std::string description;
   std::vector<dwt2d_row> rows;
   std::vector<dwt2d_tap> taps;
@@ -151,6 +152,7 @@ void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
   p.taps_per_quad = prog.taps_per_quad();
   p.left = prog.left, p.right = prog.right, p.up = prog.up, p.down = prog.down;
   p.extension = extension;
+  p.fma = prog.fused_multiply_add ? 1 : 0;
   p.rows.clear(), p.taps.clear();
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) {
@@ -180,6 +182,7 @@ StepProgram program_from_tables(const dwt2d_program& t) {
   StepProgram p;
   p.key = "program";
   p.logical_steps = t.logical_steps;
+  p.fused_multiply_add = t.fused_multiply_add != 0;
   for (int s = 0; s < t.nsteps; ++s) {
     KernelStep st;
     for (int r = 0; r < 4; ++r) {
@@ -376,6 +379,7 @@ int dwt2d_plan_get_info(const dwt2d_plan* p, dwt2d_plan_info* info) {
     info->columns_per_lane = p->entry ? p->entry->cw : 0;
     info->forward = p->forward;
     info->extension = p->extension;
+    info->fused_multiply_add = p->fma;
   });
 }
 

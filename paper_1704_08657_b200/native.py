@@ -52,7 +52,8 @@ class Tap(ctypes.Structure):
 class Program(ctypes.Structure):
     _fields_ = [("nsteps", ctypes.c_int32), ("rows", ctypes.POINTER(Row)), ("ntaps", ctypes.c_int32),
                 ("taps", ctypes.POINTER(Tap)), ("logical_steps", ctypes.c_int32),
-                ("extension", ctypes.c_int32), ("forward", ctypes.c_int32)]
+                ("extension", ctypes.c_int32), ("forward", ctypes.c_int32),
+                ("fused_multiply_add", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -62,7 +63,7 @@ class PlanInfo(ctypes.Structure):
                 ("reach_left", ctypes.c_int32), ("reach_right", ctypes.c_int32),
                 ("reach_up", ctypes.c_int32), ("reach_down", ctypes.c_int32),
                 ("columns_per_lane", ctypes.c_int32), ("forward", ctypes.c_int32),
-                ("extension", ctypes.c_int32)]
+                ("extension", ctypes.c_int32), ("fused_multiply_add", ctypes.c_int32)]
 
 
 _p = ctypes.c_void_p

@@ -30,9 +30,9 @@ def _dev(t, name="tensor"):
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
         raise TypeError(f"{name} must be a float32 CUDA tensor")
-    if t.dim() != 2 or t.stride(1) != 1:
+    if t.dim() != 2 or (t.size(1) > 1 and t.stride(1) != 1):
         raise ValueError(f"{name} must be 2-D with unit column stride")
-    return t.data_ptr(), t.stride(0)
+    return t.data_ptr(), (t.stride(0) if t.size(0) > 1 else t.size(1))
 
 
 class Plan:
@@ -53,13 +53,13 @@ class Plan:
 
     @classmethod
     def from_program(cls, rows, taps, *, logical_steps: int, forward: bool = True,
-                     extension: str = "periodic") -> "Plan":
+                     extension: str = "periodic", fma: bool = False) -> "Plan":
         """compile<float> of explicit tables: rows = [(identity, tb, te, scale)]*4*nsteps,
         taps = [(comp, dm, dn, w)]."""
         R = (N.Row * max(1, len(rows)))(*[N.Row(*r) for r in rows])
         T = (N.Tap * max(1, len(taps)))(*[N.Tap(*t) for t in taps])
         prog = N.Program(len(rows) // 4, R, len(taps), T, logical_steps, N.EXTENSIONS[extension],
-                         int(forward))
+                         int(forward), int(fma))
         self = cls.__new__(cls)
         h = ctypes.c_void_p()
         N.check(N.lib.dwt2d_plan_create_from_program(ctypes.byref(prog), ctypes.byref(h)))
@@ -69,9 +69,9 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and N is not None and getattr(N, "lib", None) is not None:
             N.lib.dwt2d_plan_destroy(h)
-            self._h = None
+        self._h = None
 
     # -- introspection -------------------------------------------------
     @property

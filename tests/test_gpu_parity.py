@@ -4,13 +4,13 @@ Oracles (test infrastructure, oracle/):
   * oracle.dwt_oracle — float64 numpy restatement of the reference path
     (pinned against the compiled reference in test_oracle.py)
   * oracle.ref        — the compiled reference itself (oracle/_ref), float32
-    and float64 executors, with and without FMA contraction
+    and float64 executors
 
 Tolerance (north star): per level, max |gpu - float64 truth|
 over the bands written at that level divided by the peak |input| of the
 level must be <= 1e-5. Composed lowerings use the reference's exact tap
-tables and accumulation order, so they are additionally compared bit for
-bit with the reference's float32 executor built with FMA contraction.
+tables, accumulation order and rounding, so they are additionally compared
+bit for bit with the reference's float32 executor.
 """
 import numpy as np
 import pytest
@@ -75,17 +75,17 @@ def test_run_planar_matches_float64_oracle(dwt, cuda, w, s, opt):
 
 
 @pytest.mark.parametrize("w,s,opt", [p for p in PLANS if not p[2]])
-def test_composed_bit_exact_vs_reference_fma(dwt, cuda, w, s, opt):
-    """Composed lowering == the reference float32 executor with FMA
-    contraction, bit for bit (same taps, same order, one rounding per tap)."""
-    if not R.available(fma=True):
+def test_composed_bit_exact_vs_reference_float32(dwt, cuda, w, s, opt):
+    """Composed lowering == the reference float32 executor, bit for bit
+    (same taps, same order, same product-then-sum rounding)."""
+    if not R.available():
         pytest.skip("oracle/_ref not built")
     plan = dwt.Plan(w, s, optimized=opt, lowering="composed")
     for (w2, h2) in [(64, 48), (33, 17), (3, 2)]:
         img = O.random_image(2 * w2, 2 * h2, 99 + w2)
         planes = O.split(img)
         got = [t.cpu().numpy() for t in plan.run(_to_dev(planes, cuda))]
-        ref, _ = R.run(w, s, planes, optimized=opt, fma=True)
+        ref, _ = R.run(w, s, planes, optimized=opt)
         for j in range(4):
             assert np.array_equal(got[j], ref[j]), (
                 f"{w}/{s} {w2}x{h2} comp {j}: {int(np.sum(got[j] != ref[j]))} samples differ, "

@@ -118,7 +118,8 @@ def test_program_tables_round_trip_through_the_abi(dwt):
     """compile() path of the C++ API: tables in, kernel found by fingerprint."""
     p = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
     rows, taps = p.tables()
-    q = dwt.Plan.from_program([(int(i), tb, te, sc) for i, tb, te, sc in rows], taps, logical_steps=4)
+    q = dwt.Plan.from_program([(int(i), tb, te, sc) for i, tb, te, sc in rows], taps, logical_steps=4,
+                              fma=True)
     assert q.info["fingerprint"] == p.info["fingerprint"]
     assert q.info["key"] == p.info["key"]
 
