@@ -111,21 +111,60 @@ __device__ __forceinline__ float fetch(const float (&v)[CW]) {
   }
 }
 
-// One sub-step on one row: out[r][c] from the input window `in`
-// (in[k] = the row k rows older than the newest input row).
-template <class P, int s, int D, int CW>
-__device__ __forceinline__ void eval_step(const float (&in)[D][4][CW], float (&out)[4][CW]) {
+// Compile-time schedule of the register windows.
+//
+// Window b holds the last rows of sub-step b's input (b = 0: loaded rows,
+// b = S: final output). Window 0 doubles as the load pipeline: it has
+// PF + depth(0) - 1 slots so the load for row i + PF can be issued into the
+// slot that row i - depth(0) + 1 just vacated. Windows are circular buffers
+// indexed by (row mod slots); the main loop is unrolled by UNR = lcm of all
+// slot counts so every slot index is a compile-time constant and rows never
+// move between registers. If that lcm is large (wide convolution windows),
+// the windows shift instead (register moves, UNR = slots of window 0).
+template <class P, int PF>
+struct Sched {
+  using M = Meta<P>;
+  static constexpr int S = M::S;
+  static constexpr int slots(int b) { return b == 0 ? PF + M::depth(0) - 1 : (b < S ? M::depth(b) : 1); }
+  static constexpr int gcd(int a, int b) { return b == 0 ? a : gcd(b, a % b); }
+  static constexpr int lcm_all() {
+    int l = 1;
+    for (int b = 0; b <= S; ++b) l = l / gcd(l, slots(b)) * slots(b);
+    return l;
+  }
+  static constexpr bool kCirc = lcm_all() <= 8;
+  static constexpr int UNR = kCirc ? lcm_all() : slots(0);
+  static constexpr int DMAX() {
+    int v = 1;
+    for (int b = 0; b <= S; ++b) v = cmax(v, slots(b));
+    return v;
+  }
+  static constexpr int D = DMAX();
+  // register slot of the row `age` rows older than the newest row of window
+  // b, at unrolled iteration u (circular mode); age itself in shift mode
+  // (window 0 is always circular: it is the load ring)
+  static constexpr int slot(int b, int u, int age) {
+    const int n = slots(b);
+    return (kCirc || b == 0) ? ((u - age) % n + n) % n : age;
+  }
+};
+
+template <class P, int PF, int s, int u, int D, int CW>
+__device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW]) {
+  using SC = Sched<P, PF>;
   constexpr int nhi = Meta<P>::nhi(s);
+  constexpr int dst = SC::slot(s + 1, u, 0);
   sfor<0, 4>([&](auto R_) {
     constexpr int r = decltype(R_)::value;
     constexpr RowDesc row = P::rows[s * 4 + r];
     if constexpr (row.ident) {
+      constexpr int src = SC::slot(s, u, nhi);
       sfor<0, CW>([&](auto C_) {
         constexpr int c = decltype(C_)::value;
-        out[r][c] = in[nhi][r][c];
+        ring[s + 1][dst][r][c] = ring[s][src][r][c];
       });
     } else if constexpr (row.tb == row.te) {  // an all-zero matrix row
-      sfor<0, CW>([&](auto C_) { out[r][decltype(C_)::value] = 0.0f; });
+      sfor<0, CW>([&](auto C_) { ring[s + 1][dst][r][decltype(C_)::value] = 0.0f; });
     } else {
       // acc = 0 + w0*v0 + w1*v1 + ... in table order. Composed programs round
       // like the reference's `acc += f.w * src` (executor.hpp:183: product
@@ -138,12 +177,12 @@ __device__ __forceinline__ void eval_step(const float (&in)[D][4][CW], float (&o
         constexpr int ti = decltype(T_)::value;
         constexpr TapDesc t = P::taps[ti];
         // scalar copies: nested lambdas may only use scalar constexpr locals
-        constexpr int k = nhi - t.dn, j = t.j, dm = t.dm;
+        constexpr int k = SC::slot(s, u, nhi - t.dn), j = t.j, dm = t.dm;
         constexpr float w = t.w;
         constexpr bool first = ti == tb;
         sfor<0, CW>([&](auto C_) {
           constexpr int c = decltype(C_)::value;
-          const float v = fetch<c + dm, CW>(in[k][j]);
+          const float v = fetch<c + dm, CW>(ring[s][k][j]);
           if constexpr (!first && P::kFma)
             acc[c] = __fmaf_rn(w, v, acc[c]);
           else if constexpr (!first)  // reference rounding: product, then sum
@@ -157,9 +196,9 @@ __device__ __forceinline__ void eval_step(const float (&in)[D][4][CW], float (&o
       sfor<0, CW>([&](auto C_) {
         constexpr int c = decltype(C_)::value;
         if constexpr (sc == 1.0f)
-          out[r][c] = acc[c];
+          ring[s + 1][dst][r][c] = acc[c];
         else
-          out[r][c] = __fmul_rn(acc[c], sc);
+          ring[s + 1][dst][r][c] = __fmul_rn(acc[c], sc);
       });
     }
   });
@@ -172,53 +211,96 @@ __device__ __forceinline__ int wrap(int i, int n) {
 
 // ------------------------------------------------------------ row I/O
 
-template <int CW, bool IL>
-__device__ __forceinline__ void load_row(const LevelArgs& a, int n, int xc, float (&d)[4][CW]) {
-  const int rr = wrap(n, a.h2);
-  if (a.vec) {
-    const int x = wrap(xc, a.w2);  // lane's CW columns never straddle the wrap (w2 % CW == 0)
-    if constexpr (IL) {
-      sfor<0, 2>([&](auto PY_) {
-        constexpr int py = decltype(PY_)::value;
-        const float* p = a.in[0] + (2ll * rr + py) * a.in_pitch[0] + 2ll * x;
-        sfor<0, CW / 2>([&](auto Q_) {
-          constexpr int q = decltype(Q_)::value;
-          const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
-          d[2 * py + 0][2 * q + 0] = v.x;
-          d[2 * py + 1][2 * q + 0] = v.y;
-          d[2 * py + 0][2 * q + 1] = v.z;
-          d[2 * py + 1][2 * q + 1] = v.w;
+// Streams input rows top to bottom with periodic wrap. Column offsets are
+// fixed per lane; the row offset advances incrementally (no division in the
+// loop).
+template <int CW, bool IL, bool VEC>
+struct RowReader {
+  const float* base[4];  // per component (planar) or the image (IL), column applied
+  long long pitch[4];    // row step in floats (IL: two image rows)
+  long long off;         // offset of the next row to load
+  int rr, h2;
+  int xs[CW];            // wrapped columns (scalar path)
+  static constexpr bool vec = VEC;
+
+  __device__ __forceinline__ void init(const LevelArgs& a, int xc, int first_row) {
+    h2 = a.h2;
+    const int x = wrap(xc, a.w2);
+    sfor<0, CW>([&](auto C_) { xs[decltype(C_)::value] = wrap(xc + decltype(C_)::value, a.w2); });
+    sfor<0, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      if constexpr (IL) {
+        base[j] = a.in[0] + (vec ? 2ll * x : 0ll);
+        pitch[j] = 2ll * a.in_pitch[0];
+      } else {
+        base[j] = a.in[j] + (vec ? (long long)x : 0ll);
+        pitch[j] = a.in_pitch[j];
+      }
+    });
+    rr = wrap(first_row, h2);
+    off = (long long)rr * pitch[0];
+  }
+
+  __device__ __forceinline__ void advance() {
+    if (++rr == h2) {
+      rr = 0;
+      off = 0;
+    } else {
+      off += pitch[0];
+    }
+  }
+
+  // planar rows may have different pitches per component
+  __device__ __forceinline__ long long row_off(int j) const {
+    if constexpr (IL) return off;
+    else return j == 0 ? off : (long long)rr * pitch[j];
+  }
+
+  __device__ __forceinline__ void load(float (&d)[4][CW], const long long half_pitch) {
+    if constexpr (VEC) {
+      if constexpr (IL) {
+        sfor<0, 2>([&](auto PY_) {
+          constexpr int py = decltype(PY_)::value;
+          const float* p = base[0] + off + (py ? half_pitch : 0ll);
+          sfor<0, CW / 2>([&](auto Q_) {
+            constexpr int q = decltype(Q_)::value;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
+            d[2 * py + 0][2 * q + 0] = v.x;
+            d[2 * py + 1][2 * q + 0] = v.y;
+            d[2 * py + 0][2 * q + 1] = v.z;
+            d[2 * py + 1][2 * q + 1] = v.w;
+          });
+        });
+      } else {
+        sfor<0, 4>([&](auto J_) {
+          constexpr int j = decltype(J_)::value;
+          const float* p = base[j] + row_off(j);
+          if constexpr (CW == 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+            d[j][0] = v.x, d[j][1] = v.y, d[j][2] = v.z, d[j][3] = v.w;
+          } else if constexpr (CW == 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+            d[j][0] = v.x, d[j][1] = v.y;
+          } else {
+            sfor<0, CW>([&](auto C_) { d[j][decltype(C_)::value] = __ldg(p + decltype(C_)::value); });
+          }
+        });
+      }
+    } else {
+      sfor<0, CW>([&](auto C_) {
+        constexpr int c = decltype(C_)::value;
+        sfor<0, 4>([&](auto J_) {
+          constexpr int j = decltype(J_)::value;
+          if constexpr (IL)
+            d[j][c] = __ldg(base[0] + off + ((j >> 1) ? half_pitch : 0ll) + 2 * xs[c] + (j & 1));
+          else
+            d[j][c] = __ldg(base[j] + row_off(j) + xs[c]);
         });
       });
-    } else {
-      sfor<0, 4>([&](auto J_) {
-        constexpr int j = decltype(J_)::value;
-        const float* p = a.in[j] + (long long)rr * a.in_pitch[j] + x;
-        if constexpr (CW == 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-          d[j][0] = v.x, d[j][1] = v.y, d[j][2] = v.z, d[j][3] = v.w;
-        } else if constexpr (CW == 2) {
-          const float2 v = __ldg(reinterpret_cast<const float2*>(p));
-          d[j][0] = v.x, d[j][1] = v.y;
-        } else {
-          sfor<0, CW>([&](auto C_) { d[j][decltype(C_)::value] = __ldg(p + decltype(C_)::value); });
-        }
-      });
     }
-  } else {
-    sfor<0, CW>([&](auto C_) {
-      constexpr int c = decltype(C_)::value;
-      const int x = wrap(xc + c, a.w2);
-      sfor<0, 4>([&](auto J_) {
-        constexpr int j = decltype(J_)::value;
-        if constexpr (IL)
-          d[j][c] = __ldg(a.in[0] + (2ll * rr + (j >> 1)) * a.in_pitch[0] + 2ll * x + (j & 1));
-        else
-          d[j][c] = __ldg(a.in[j] + (long long)rr * a.in_pitch[j] + x);
-      });
-    });
+    advance();
   }
-}
+};
 
 __device__ __forceinline__ void st_vec(float* p, float4 v, bool stream) {
   if (stream) __stcs(reinterpret_cast<float4*>(p), v);
@@ -229,58 +311,88 @@ __device__ __forceinline__ void st_vec(float* p, float2 v, bool stream) {
   else *reinterpret_cast<float2*>(p) = v;
 }
 
-template <int CW, bool IL>
-__device__ __forceinline__ void store_row(const LevelArgs& a, int y, int xc, const float (&v)[4][CW]) {
-  if (a.vec) {
-    if (xc + CW > a.w2) return;
-    if constexpr (IL) {
-      sfor<0, 2>([&](auto PY_) {
-        constexpr int py = decltype(PY_)::value;
-        float* p = a.out[0] + (2ll * y + py) * a.out_pitch[0] + 2ll * xc;
-        sfor<0, CW / 2>([&](auto Q_) {
-          constexpr int q = decltype(Q_)::value;
-          st_vec(p + 4 * q,
-                 make_float4(v[2 * py][2 * q], v[2 * py + 1][2 * q], v[2 * py][2 * q + 1],
-                             v[2 * py + 1][2 * q + 1]),
-                 false);
-        });
-      });
-    } else {
-      sfor<0, 4>([&](auto J_) {
-        constexpr int j = decltype(J_)::value;
-        float* p = a.out[j] + (long long)y * a.out_pitch[j] + xc;
-        if constexpr (CW == 4)
-          st_vec(p, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
-        else if constexpr (CW == 2)
-          st_vec(p, make_float2(v[j][0], v[j][1]), j != 0);
-        else
-          sfor<0, CW>([&](auto C_) { p[decltype(C_)::value] = v[j][decltype(C_)::value]; });
-      });
-    }
-  } else {
-    sfor<0, CW>([&](auto C_) {
-      constexpr int c = decltype(C_)::value;
-      const int x = xc + c;
-      if (x < a.w2) {
-        sfor<0, 4>([&](auto J_) {
-          constexpr int j = decltype(J_)::value;
-          if constexpr (IL)
-            a.out[0][(2ll * y + (j >> 1)) * a.out_pitch[0] + 2ll * x + (j & 1)] = v[j][c];
-          else
-            a.out[j][(long long)y * a.out_pitch[j] + x] = v[j][c];
-        });
+// Writes output rows y0, y0 + 1, ... (no wrap); pointers advance per row.
+template <int CW, bool IL, bool VEC>
+struct RowWriter {
+  float* p[4];
+  long long pitch[4];
+  int xc, w2;
+
+  __device__ __forceinline__ void init(const LevelArgs& a, int xc_, int first_row) {
+    xc = xc_, w2 = a.w2;
+    sfor<0, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      if constexpr (IL) {
+        pitch[j] = a.out_pitch[0];
+        p[j] = a.out[0] + 2ll * first_row * a.out_pitch[0] + 2ll * xc;
+      } else {
+        pitch[j] = a.out_pitch[j];
+        p[j] = a.out[j] + (long long)first_row * a.out_pitch[j] + xc;
       }
     });
   }
-}
+
+  __device__ __forceinline__ void advance() {
+    if constexpr (IL) {
+      p[0] += 2 * pitch[0];
+    } else {
+      sfor<0, 4>([&](auto J_) { p[decltype(J_)::value] += pitch[decltype(J_)::value]; });
+    }
+  }
+
+  // whether this lane's columns are inside the image (fixed per lane)
+  __device__ __forceinline__ bool lane_in_range() const { return VEC ? xc + CW <= w2 : xc < w2; }
+
+  __device__ __forceinline__ void store(const float (&v)[4][CW]) {
+    if constexpr (VEC) {
+      if constexpr (IL) {
+        sfor<0, 2>([&](auto PY_) {
+          constexpr int py = decltype(PY_)::value;
+          float* q = p[0] + (py ? pitch[0] : 0ll);
+          sfor<0, CW / 2>([&](auto Q_) {
+            constexpr int k = decltype(Q_)::value;
+            st_vec(q + 4 * k,
+                   make_float4(v[2 * py][2 * k], v[2 * py + 1][2 * k], v[2 * py][2 * k + 1],
+                               v[2 * py + 1][2 * k + 1]),
+                   false);
+          });
+        });
+      } else {
+        sfor<0, 4>([&](auto J_) {
+          constexpr int j = decltype(J_)::value;
+          if constexpr (CW == 4)
+            st_vec(p[j], make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
+          else if constexpr (CW == 2)
+            st_vec(p[j], make_float2(v[j][0], v[j][1]), j != 0);
+          else
+            sfor<0, CW>([&](auto C_) { p[j][decltype(C_)::value] = v[j][decltype(C_)::value]; });
+        });
+      }
+    } else {
+      sfor<0, CW>([&](auto C_) {
+        constexpr int c = decltype(C_)::value;
+        if (xc + c < w2) {
+          sfor<0, 4>([&](auto J_) {
+            constexpr int j = decltype(J_)::value;
+            if constexpr (IL)
+              p[0][((j >> 1) ? pitch[0] : 0ll) + 2 * c + (j & 1)] = v[j][c];
+            else
+              p[j][c] = v[j][c];
+          });
+        }
+      });
+    }
+  }
+};
 
 // ------------------------------------------------------------- kernel
 
-template <class P, int PF, bool IN_IL, bool OUT_IL>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
 level_kernel(const LevelArgs a) {
   using M = Meta<P>;
-  constexpr int S = M::S, CW = M::CW, D = M::D;
+  using SC = Sched<P, PF>;
+  constexpr int S = M::S, CW = M::CW, D = SC::D, UNR = SC::UNR, NS0 = SC::slots(0);
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
@@ -288,12 +400,14 @@ level_kernel(const LevelArgs a) {
   const int xc = (strip * kOutLanes - 1 + lane) * CW;  // first component column of this lane
   const int y0 = chunk * a.chunk_rows;
   const int y1 = min(a.h2, y0 + a.chunk_rows);
-  const int n0 = y0 - M::U;
-  const int iters = (y1 - y0) + M::U + M::L;
-  const bool out_lane = lane >= 1 && lane <= kOutLanes;
+  const int n0 = y0 - M::U;  // first input row streamed
+  const int rows = (y1 - y0) + M::U + M::L;
+  const int iters = (rows + UNR - 1) / UNR * UNR;
+  bool out_lane = lane >= 1 && lane <= kOutLanes;
+  const long long half_pitch = IN_IL ? a.in_pitch[0] : 0;
 
   float ring[S + 1][D][4][CW];
-  sfor<0, S + 1>([&](auto B_) {
+  sfor<1, S + 1>([&](auto B_) {
     sfor<0, D>([&](auto K_) {
       sfor<0, 4>([&](auto J_) {
         sfor<0, CW>([&](auto C_) {
@@ -302,21 +416,26 @@ level_kernel(const LevelArgs a) {
       });
     });
   });
-  float pf[PF][4][CW];
+
+  RowReader<CW, IN_IL, VEC> rd;
+  rd.init(a, xc, n0);
+  RowWriter<CW, OUT_IL, VEC> wr;
+  wr.init(a, xc, n0 - M::L);
+  out_lane = out_lane && wr.lane_in_range();
+  // prologue: rows n0 .. n0+PF-1 land in the slots iteration 0.. expect
   sfor<0, PF>([&](auto U_) {
     constexpr int u = decltype(U_)::value;
-    if (u < iters) load_row<CW, IN_IL>(a, n0 + u, xc, pf[u]);
+    rd.load(ring[0][SC::slot(0, u, 0)], half_pitch);
   });
 
-  for (int it = 0; it < iters; it += PF) {
-    sfor<0, PF>([&](auto U_) {
+  for (int it = 0; it < iters; it += UNR) {
+    sfor<0, UNR>([&](auto U_) {
       constexpr int u = decltype(U_)::value;
       const int i = it + u;
-      if (i < iters) {  // warp-uniform
-        // age every window by one row
-        sfor<0, S + 1>([&](auto B_) {
+      if constexpr (!SC::kCirc) {  // shift windows 1..S by one row
+        sfor<1, S + 1>([&](auto B_) {
           constexpr int b = decltype(B_)::value;
-          constexpr int dep = M::depth(b);
+          constexpr int dep = SC::slots(b);
           sfor<1, dep>([&](auto K_) {
             constexpr int k = dep - decltype(K_)::value;  // dep-1 .. 1
             sfor<0, 4>([&](auto J_) {
@@ -327,22 +446,17 @@ level_kernel(const LevelArgs a) {
             });
           });
         });
-        sfor<0, 4>([&](auto J_) {
-          sfor<0, CW>([&](auto C_) {
-            ring[0][0][decltype(J_)::value][decltype(C_)::value] =
-                pf[u][decltype(J_)::value][decltype(C_)::value];
-          });
-        });
-        if (i + PF < iters) load_row<CW, IN_IL>(a, n0 + i + PF, xc, pf[u]);
-        sfor<0, S>([&](auto S_) {
-          constexpr int s = decltype(S_)::value;
-          eval_step<P, s, D, CW>(ring[s], ring[s + 1][0]);
-        });
-        const int y = n0 + i - M::L;
-        if (y >= y0 && out_lane) store_row<CW, OUT_IL>(a, y, xc, ring[S][0]);
       }
+      eval_step<P, PF, 0, u, D, CW>(ring);
+      // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
+      if (i + PF < rows) rd.load(ring[0][SC::slot(0, u, -PF)], half_pitch);
+      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW>(ring); });
+      const int y = n0 + i - M::L;
+      if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
+      wr.advance();
     });
   }
+  (void)NS0;
 }
 
 }  // namespace gpu

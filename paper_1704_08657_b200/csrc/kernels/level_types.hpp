@@ -39,6 +39,8 @@ struct LevelArgs {
 };
 
 using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
+// resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
+using LevelOccupancy = int (*)();
 
 struct PlanEntry {
   const char* key;
@@ -49,6 +51,7 @@ struct PlanEntry {
   LevelLaunch planar;          // 4 planes -> 4 planes   (run() API)
   LevelLaunch from_image;      // interleaved -> 4 planes (forward levels)
   LevelLaunch to_image;        // 4 planes -> interleaved (inverse levels)
+  LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
 };
 
 const std::vector<PlanEntry>& plan_registry();

@@ -21,8 +21,22 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   const long long warps = (long long)a.nstrips * a.nchunks;
   if (warps <= 0) return cudaSuccess;
   const unsigned blocks = unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta);
-  level_kernel<P, kPrefetchRows, IN_IL, OUT_IL><<<blocks, kWarpsPerCta * 32, 0, st>>>(a);
+  if (a.vec)
+    level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true><<<blocks, kWarpsPerCta * 32, 0, st>>>(a);
+  else
+    level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, false><<<blocks, kWarpsPerCta * 32, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+template <class P, bool IN_IL, bool OUT_IL>
+int level_occupancy() {
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &blocks, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true>, kWarpsPerCta * 32, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return blocks;
 }
 
 template <class P, bool kForward>
@@ -35,10 +49,13 @@ PlanEntry make_entry() {
   e.up = M::U, e.down = M::L, e.left = M::HL, e.right = M::HR;
   e.taps_per_quad = P::kTaps;
   e.planar = &launch_level<P, false, false>;
-  if constexpr (kForward)
+  if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;
-  else
+    e.occupancy = &level_occupancy<P, true, false>;
+  } else {
     e.to_image = &launch_level<P, false, true>;
+    e.occupancy = &level_occupancy<P, false, true>;
+  }
   return e;
 }
 

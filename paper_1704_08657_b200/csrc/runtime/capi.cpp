@@ -94,20 +94,30 @@ int sm_count() {
 
 bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
 
-// Rows per warp work item: enough items for ~4 waves of 16 warps per SM,
-// but long enough that the (up + down) warm-up rows stay a small overhead.
-int chunk_rows_for(const dwt2d_plan& p, int w2, int h2, int nstrips) {
+// Rows per warp work item. A warp streams one strip of one chunk; the
+// (up + down) rows around each chunk are re-read as warm-up. Measured on
+// B200 (scripts/tune_level.cu): large levels run best with ~5 waves of work
+// items (chunk ~64 rows at 16384^2: 6.1 TB/s) — many short items keep
+// vertically adjacent chunks in flight together so their shared halo rows
+// hit L2 — while small, L2-resident levels are latency bound and want more
+// warps (chunks of 2..8 rows).
+int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
   if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
     const int v = std::atoi(env);
     if (v > 0) return v;
   }
-  const long long target = 4ll * 16 * sm_count();
-  const long long per_strip = std::max<long long>(1, target / std::max(1, nstrips));
-  int chunk = int((h2 + per_strip - 1) / per_strip);
-  const int floor_rows = std::max(8, 4 * (p.up + p.down));
-  chunk = std::max(chunk, std::min(floor_rows, h2));
-  chunk = std::min(chunk, 512);
-  return std::max(1, chunk);
+  static thread_local const gpu::PlanEntry* cached_entry = nullptr;
+  static thread_local int cached_blocks = 0;
+  if (cached_entry != p.entry) {
+    cached_entry = p.entry;
+    cached_blocks = p.entry->occupancy ? p.entry->occupancy() : 0;
+  }
+  const long long resident = std::max(1, cached_blocks ? cached_blocks : 2) * 4ll * sm_count();
+  const long long rows_total = (long long)h2 * std::max(1, nstrips);
+  const int for_waves = int((rows_total + 5 * resident - 1) / (5 * resident));   // ~5 waves
+  const int for_fill = int(std::max(2ll, (rows_total + resident - 1) / resident));  // >= 1 wave
+  const int chunk = std::max(for_waves, std::min(8, for_fill));
+  return std::max(1, std::min(chunk, h2));
 }
 
 enum Layout { kPlanar, kFromImage, kToImage };
@@ -117,7 +127,7 @@ void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t s
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
-  a.chunk_rows = chunk_rows_for(p, a.w2, a.h2, a.nstrips);
+  a.chunk_rows = chunk_rows_for(p, a.h2, a.nstrips);
   a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
   bool vec = a.w2 % cw == 0;
   const bool in_il = layout == kFromImage, out_il = layout == kToImage;

@@ -1,0 +1,95 @@
+// Tuning harness (development only): times variants of the headline level
+// kernel (cdf97 non-separable lifting, optimized) on a 16384^2 image:
+// columns per lane, prefetch depth, minimum resident CTAs, chunk rows.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20
+//        --expt-relaxed-constexpr -I include scripts/tune_level.cu -o build/tune_level
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1704_08657_b200/csrc/generated/plans_gen.cuh"
+#include "../paper_1704_08657_b200/csrc/kernels/level_engine.cuh"
+
+using namespace dwt2d_b200::gpu;
+
+template <class Base, int CW_>
+struct WithCW : Base {
+  static constexpr int kCW = CW_;
+};
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+__global__ void fill(float* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = (float)((i * 2654435761ull) % 1000003ull) * 1e-6f;
+}
+
+template <class P, int PF, int MINB>
+void run(const char* name, float* img, float* out[4], int W, int H, int chunk, const float* ref, float* host) {
+  using Pl = P;
+  LevelArgs a{};
+  for (int j = 0; j < 4; ++j) {
+    a.in[j] = img, a.in_pitch[j] = W;
+    a.out[j] = out[j], a.out_pitch[j] = W / 2;
+  }
+  a.w2 = W / 2, a.h2 = H / 2;
+  a.nstrips = (a.w2 + kOutLanes * Pl::kCW - 1) / (kOutLanes * Pl::kCW);
+  a.chunk_rows = chunk;
+  a.nchunks = (a.h2 + chunk - 1) / chunk;
+  a.vec = 1;
+  const long long warps = (long long)a.nstrips * a.nchunks;
+  const unsigned blocks = unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta);
+  auto k = level_kernel<Pl, PF, true, false, true, MINB>;
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, k));
+  for (int i = 0; i < 3; ++i) k<<<blocks, 128>>>(a);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0), cudaEventCreate(&e1);
+  const int iters = 20;
+  cudaEventRecord(e0);
+  for (int i = 0; i < iters; ++i) k<<<blocks, 128>>>(a);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= iters;
+  const double gbs = 8.0 * W * (double)H / (ms * 1e-3) / 1e9;
+  // correctness vs reference variant output (same arithmetic => same bits)
+  long long bad = 0;
+  if (ref) {
+    const size_t n = size_t(W / 2) * (H / 2);
+    CK(cudaMemcpy(host, out[3], n * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) bad += host[i] != ref[i];
+  }
+  printf("%-20s W=%5d cw=%d pf=%d minb=%d chunk=%4d warps=%6lld regs=%3d  %8.2f us  %7.1f GB/s  mismatches=%lld\n",
+         name, W, Pl::kCW, PF, MINB, chunk, warps, fa.numRegs, ms * 1e3, gbs, bad);
+}
+
+int main(int argc, char** argv) {
+  const int W = 16384, H = 16384;
+  float* img;
+  CK(cudaMalloc(&img, size_t(W) * H * 4));
+  fill<<<1184, 256>>>(img, (long long)W * H);
+  float* out[4];
+  for (int j = 0; j < 4; ++j) CK(cudaMalloc(&out[j], size_t(W / 2) * (H / 2) * 4));
+  const size_t n = size_t(W / 2) * (H / 2);
+  std::vector<float> ref(n), host(n);
+  using P = plans::cdf97_nonseparable_lifting_opt;
+  run<WithCW<P, 4>, 2, 1>("base cw4", img, out, W, H, 64, nullptr, nullptr);
+  CK(cudaMemcpy(ref.data(), out[3], n * 4, cudaMemcpyDeviceToHost));
+  for (int chunk : {48, 64, 96, 328, 342}) {
+    run<WithCW<P, 4>, 2, 1>("cw4 pf2", img, out, W, H, chunk, ref.data(), host.data());
+    run<WithCW<P, 4>, 3, 1>("cw4 pf3", img, out, W, H, chunk, ref.data(), host.data());
+    run<WithCW<P, 2>, 4, 4>("cw2 pf4 minb4", img, out, W, H, chunk, ref.data(), host.data());
+  }
+  // small (deep-level) shapes: latency bound
+  for (int sz : {4096, 2048, 1024, 512, 256}) {
+    for (int chunk : {2, 4, 8, 16}) {
+      run<WithCW<P, 4>, 2, 1>("small cw4 pf2", img, out, sz, sz, chunk, nullptr, nullptr);
+      run<WithCW<P, 2>, 4, 4>("small cw2 pf4", img, out, sz, sz, chunk, nullptr, nullptr);
+    }
+  }
+  // plain copy kernel for the same bytes as a sanity ceiling
+  return 0;
+}
