@@ -170,6 +170,117 @@ def run_reference_arm(args):
     return 0
 
 
+UP = DOWN = 2  # CDF 9/7 level reach in component rows (halo = 4 image rows each side)
+
+
+def run_single(args, plan, img, out, dev):
+    """N = 1: K pyramids captured in one CUDA graph, events between levels."""
+    import torch
+    import paper_1704_08657_b200 as dwt
+    W = H = SIZE
+    scratch = torch.empty(dwt.workspace_bytes(W, H, LEVELS) // 4 + 64, dtype=torch.float32, device=dev)
+
+    # per-level views: LL_l lives in scratch (ping-pong), bands in the Mallat buffer
+    views = []
+    src = img
+    a_pad = ((W // 2) * (H // 2) + 63) // 64 * 64
+    for lvl in range(1, LEVELS + 1):
+        w, h = W >> (lvl - 1), H >> (lvl - 1)
+        w2, h2 = w // 2, h // 2
+        if lvl == LEVELS:
+            ll = out[:h2, :w2]
+        else:
+            base = 0 if lvl % 2 == 1 else a_pad
+            ll = scratch[base:base + w2 * h2].view(h2, w2)
+        views.append((src, [ll, out[:h2, w2:w], out[h2:h, :w2], out[h2:h, w2:w]]))
+        src = ll
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(events=None):
+        for lvl, (src, bands) in enumerate(views):
+            if events is not None:
+                events[lvl].record(stream)
+            plan.forward_level(src, bands, stream=stream.cuda_stream)
+        if events is not None:
+            events[LEVELS].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    stream.synchronize()
+    ref_out = plan.forward_mallat(img, LEVELS, scratch=scratch)
+    torch.cuda.synchronize()
+    assert torch.equal(ref_out, out), "per-level driver and forward_mallat disagree"
+
+    evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(LEVELS + 1)]
+           for _ in range(args.steps)]
+    graph = torch.cuda.CUDAGraph()
+    launches0 = dwt.launch_count()
+    with torch.cuda.graph(graph, stream=stream):
+        for k in range(args.steps):
+            step(evs[k])
+    launches = dwt.launch_count() - launches0
+    with torch.cuda.stream(stream):
+        graph.replay()  # untimed replay warms the graph
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
+        t0.record(stream)
+        graph.replay()  # replays on the current stream (= `stream` here)
+        t1.record(stream)
+        t1.synchronize()
+    torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    level_ms = [statistics.mean(e[l].elapsed_time(e[l + 1]) for e in evs) for l in range(LEVELS)]
+    ms_per_step = total_ms / args.steps
+    return SIZE * SIZE / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
+
+
+def run_sharded(args, plan, img, out, dev, n):
+    """N > 1: each rank owns a 16384-row strip; every level exchanges 4+4
+    halo rows with its ring neighbours (NCCL) and runs the fused strip
+    kernel. Eager launches (NCCL P2P per level), events around each level."""
+    import torch
+    import torch.distributed as dist
+    import paper_1704_08657_b200 as dwt
+    from paper_1704_08657_b200 import strips as S
+    ex = S.HaloExchange()
+    cur_events = []
+
+    def level_fn(cur, top, bottom):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = plan.forward_level_strip(cur, top, bottom)
+        e1.record()
+        cur_events.append((e0, e1))
+        return r
+
+    for _ in range(args.warmup):
+        S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out)
+    torch.cuda.synchronize()
+    cur_events.clear()
+    launches0 = dwt.launch_count()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out)
+        t1.record()
+        t1.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+    launches = dwt.launch_count() - launches0
+    total = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+    level_ms = [statistics.mean(cur_events[k * LEVELS + l][0].elapsed_time(cur_events[k * LEVELS + l][1])
+                                for k in range(args.steps)) for l in range(LEVELS)]
+    return SIZE * SIZE * n / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -199,101 +310,45 @@ def main():
     # this rank's strip: rows [rank*H, (rank+1)*H) of the W x (n*H) image
     img = random_image(W, H * n, 1, row0=rank * H, rows=H, device=dev)
     out = torch.empty_like(img)
-    scratch = torch.empty(dwt.workspace_bytes(W, H, LEVELS) // 4 + 64, dtype=torch.float32, device=dev)
-
-    # per-level views: LL_l lives in scratch (ping-pong), bands in the Mallat buffer
-    def level_views():
-        views = []
-        src = img
-        a_elems = (W // 2) * (H // 2)
-        a_pad = (a_elems + 63) // 64 * 64
-        for lvl in range(1, LEVELS + 1):
-            w, h = W >> (lvl - 1), H >> (lvl - 1)
-            w2, h2 = w // 2, h // 2
-            if lvl == LEVELS:
-                ll = out[:h2, :w2]
-            else:
-                base = 0 if lvl % 2 == 1 else a_pad
-                ll = scratch[base:base + w2 * h2].view(h2, w2)
-            bands = [ll, out[:h2, w2:w], out[h2:h, :w2], out[h2:h, w2:w]]
-            views.append((src, bands))
-            src = ll
-        return views
-
-    views = level_views()
-    stream = torch.cuda.Stream(device=dev)
-
-    def step(events=None):
-        for lvl, (src, bands) in enumerate(views):
-            if events is not None:
-                events[lvl].record(stream)
-            plan.forward_level(src, bands, stream=stream.cuda_stream)
-        if events is not None:
-            events[LEVELS].record(stream)
-
-    # warm-up (also proves the multi-level API gives the same bits)
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-    stream.synchronize()
-    ref_out = plan.forward_mallat(img, LEVELS, scratch=scratch)
-    torch.cuda.synchronize()
-    assert torch.equal(ref_out, out), "per-level driver and forward_mallat disagree"
-
-    # capture K steps with per-level events into one graph
-    evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(LEVELS + 1)]
-           for _ in range(args.steps)]
-    graph = torch.cuda.CUDAGraph()
-    launches0 = dwt.launch_count()
-    with torch.cuda.graph(graph, stream=stream):
-        for k in range(args.steps):
-            step(evs[k])
-    launches_captured = dwt.launch_count() - launches0
-    with torch.cuda.stream(stream):
-        graph.replay()  # untimed replay warms the graph
-    torch.cuda.synchronize()
-
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if n > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk, torch.cuda.stream(stream):
-        t0.record(stream)
-        graph.replay()  # replays on the current stream (= `stream` here)
-        t1.record(stream)
-        t1.synchronize()
-        if n > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-    total_ms = t0.elapsed_time(t1)
-    level_ms = [statistics.mean(e[l].elapsed_time(e[l + 1]) for e in evs) for l in range(LEVELS)]
-    if n > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+        value, ms_per_step, level_ms, launches_captured, clk = run_sharded(args, plan, img, out, dev, n)
+    else:
+        value, ms_per_step, level_ms, launches_captured, clk = run_single(args, plan, img, out, dev)
     pixels = W * H * n
-    value = pixels / (ms_per_step * 1e-3) / 1e9
 
     # end to end through the C ABI host entry point: pinned host image ->
     # H2D -> 8 levels -> D2H of the whole pyramid, synchronous per step
     host_img = img.cpu().pin_memory()
     host_out = torch.empty_like(host_img).pin_memory()
-    hi, ho = host_img.numpy(), host_out.numpy()
-    plan.forward_mallat_host(hi, LEVELS, ho)
+    if n == 1:
+        hi, ho = host_img.numpy(), host_out.numpy()
+
+        def e2e_step():
+            plan.forward_mallat_host(hi, LEVELS, ho)
+    else:
+        from paper_1704_08657_b200 import strips as S
+        ex = S.HaloExchange()
+        dev_in, dev_out = torch.empty_like(img), torch.empty_like(img)
+
+        def e2e_step():
+            dev_in.copy_(host_img, non_blocking=True)
+            S.forward_mallat_strips(S.gpu_level_fn(plan), dev_in, LEVELS, UP, DOWN, ex, out=dev_out)
+            host_out.copy_(dev_out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+    e2e_step()
     if n > 1:
         dist.barrier()
     e2e_t = []
     for _ in range(args.e2e_steps):
         a = time.perf_counter()
-        plan.forward_mallat_host(hi, LEVELS, ho)
+        e2e_step()
         e2e_t.append(time.perf_counter() - a)
     e2e_s = statistics.median(e2e_t)
     if n > 1:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    assert torch.equal(host_out.to(dev), out), "host entry point disagrees with device pyramid"
+    assert torch.equal(host_out.to(dev), out), "end-to-end entry point disagrees with device pyramid"
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -315,7 +370,7 @@ def main():
             "data": "synthetic (reference LCG random_image, seed 1, generated on device with jump-ahead)",
             "config": workload_config(n),
             "ns_per_pixel": ms_per_step * 1e6 / pixels,
-            "pyramid_hbm_gbs": pyr_bytes * n / (ms_per_step * 1e-3) / 1e9 / n,
+            "pyramid_hbm_gbs_per_gpu": pyr_bytes / (ms_per_step * 1e-3) / 1e9,
             "levels_ms": [round(x, 5) for x in level_ms],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(),
@@ -323,8 +378,12 @@ def main():
                          "peak_source": peak_src},
             "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
                     "h2d_bytes_per_step": int(W * H * 4), "d2h_bytes_per_step": int(W * H * 4),
-                    "api": "dwt2d_forward_mallat_host (C ABI), pinned host buffers"},
+                    "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if n == 1 else
+                            "pinned host strip -> H2D -> strips.forward_mallat_strips (C ABI strip "
+                            "kernel + NCCL halos) -> D2H, per rank")},
             "gpu_launches": int(launches_captured),
+            "halo_exchange": ("NCCL batched send/recv of 4+4 image rows per level per rank (ring)"
+                              if n > 1 else None),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -147,6 +147,27 @@ DWT2D_B200_API int dwt2d_inverse_level(const dwt2d_plan* plan, const float* cons
                                        const size_t in_pitch[4], float* image, size_t pitch,
                                        int width, int height, void* stream);
 
+/* --- row strips of a sharded image (multi-GPU) ---------------
+ * One forward level of a strip of `height` image rows of a larger image whose
+ * rows above and below live elsewhere (another GPU): `top` holds the
+ * 2*reach_up image rows directly above the strip, `bottom` the 2*reach_down
+ * rows directly below (dwt2d_plan_info; 4 and 4 for CDF 9/7), both with
+ * `halo_pitch`. Periodic wrap of the whole image is the caller's choice of
+ * neighbours (ring). Output: the strip's rows of the four bands. */
+DWT2D_B200_API int dwt2d_forward_level_strip(const dwt2d_plan* plan, const float* image, size_t pitch,
+                                             int width, int height, const float* top,
+                                             const float* bottom, size_t halo_pitch,
+                                             float* const out[4], const size_t out_pitch[4],
+                                             void* stream);
+/* Inverse counterpart: four planar band strips (w2 x h2) plus reach_up rows
+ * above and reach_down rows below of each band (top[j], bottom[j]) into the
+ * strip's 2*h2 image rows. */
+DWT2D_B200_API int dwt2d_inverse_level_strip(const dwt2d_plan* plan, const float* const in[4],
+                                             const size_t in_pitch[4], const float* const top[4],
+                                             const float* const bottom[4],
+                                             const size_t halo_pitch[4], float* image, size_t pitch,
+                                             int width, int height, void* stream);
+
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by
  * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL

@@ -211,57 +211,66 @@ __device__ __forceinline__ int wrap(int i, int n) {
 
 // ------------------------------------------------------------ row I/O
 
-// Streams input rows top to bottom with periodic wrap. Column offsets are
-// fixed per lane; the row offset advances incrementally (no division in the
-// loop).
+// Streams input rows top to bottom. Row n (relative to the chunk's level)
+// comes from the main input with periodic wrap, or — for a row strip of a
+// sharded image — from the halo buffers above/below the strip. Column offsets
+// are fixed per lane; the row pointer advances by one pitch per row and is
+// recomputed only when the row crosses a segment boundary (no division in
+// the steady state).
 template <int CW, bool IL, bool VEC>
 struct RowReader {
-  const float* base[4];  // per component (planar) or the image (IL), column applied
-  long long pitch[4];    // row step in floats (IL: two image rows)
-  long long off;         // offset of the next row to load
-  int rr, h2;
-  int xs[CW];            // wrapped columns (scalar path)
-  static constexpr bool vec = VEC;
+  static constexpr int NP = IL ? 1 : 4;  // row pointers kept
+  const float* rowp[NP];  // start of the current row (+ lane column for VEC)
+  long long pitch[NP];    // current segment's row step (IL: two image rows)
+  long long half;         // IL: offset of the odd image row within a component row
+  int n, next_switch;
+  int xs[CW];             // wrapped columns (scalar path)
+  int xv;                 // wrapped first column (vector path)
 
-  __device__ __forceinline__ void init(const LevelArgs& a, int xc, int first_row) {
-    h2 = a.h2;
-    const int x = wrap(xc, a.w2);
-    sfor<0, CW>([&](auto C_) { xs[decltype(C_)::value] = wrap(xc + decltype(C_)::value, a.w2); });
-    sfor<0, 4>([&](auto J_) {
+  __device__ __forceinline__ void seek(const LevelArgs& a, int row) {
+    n = row;
+    const float* const* src = a.in;
+    const long long* sp = a.in_pitch;
+    int r = row;
+    if (a.halo && row < 0) {
+      src = a.halo_top, sp = a.halo_top_pitch, r = row + a.up;
+      next_switch = 0;
+    } else if (a.halo && row >= a.h2) {
+      src = a.halo_bot, sp = a.halo_bot_pitch, r = row - a.h2;
+      next_switch = 0x7fffffff;
+    } else {
+      r = a.halo ? row : wrap(row, a.h2);
+      next_switch = a.halo ? a.h2 : row - r + a.h2;
+    }
+    sfor<0, NP>([&](auto J_) {
       constexpr int j = decltype(J_)::value;
-      if constexpr (IL) {
-        base[j] = a.in[0] + (vec ? 2ll * x : 0ll);
-        pitch[j] = 2ll * a.in_pitch[0];
-      } else {
-        base[j] = a.in[j] + (vec ? (long long)x : 0ll);
-        pitch[j] = a.in_pitch[j];
-      }
+      const long long step = IL ? 2ll * sp[0] : sp[j];
+      pitch[j] = step;
+      rowp[j] = src[j] + (long long)r * step + (VEC ? (IL ? 2ll * xv : (long long)xv) : 0ll);
     });
-    rr = wrap(first_row, h2);
-    off = (long long)rr * pitch[0];
+    if constexpr (IL) half = sp[0];
   }
 
-  __device__ __forceinline__ void advance() {
-    if (++rr == h2) {
-      rr = 0;
-      off = 0;
+  __device__ __forceinline__ void init(const LevelArgs& a, int xc, int first_row) {
+    xv = wrap(xc, a.w2);
+    sfor<0, CW>([&](auto C_) { xs[decltype(C_)::value] = wrap(xc + decltype(C_)::value, a.w2); });
+    seek(a, first_row);
+  }
+
+  __device__ __forceinline__ void advance(const LevelArgs& a) {
+    if (++n == next_switch) {
+      seek(a, n);
     } else {
-      off += pitch[0];
+      sfor<0, NP>([&](auto J_) { rowp[decltype(J_)::value] += pitch[decltype(J_)::value]; });
     }
   }
 
-  // planar rows may have different pitches per component
-  __device__ __forceinline__ long long row_off(int j) const {
-    if constexpr (IL) return off;
-    else return j == 0 ? off : (long long)rr * pitch[j];
-  }
-
-  __device__ __forceinline__ void load(float (&d)[4][CW], const long long half_pitch) {
+  __device__ __forceinline__ void load(const LevelArgs& a, float (&d)[4][CW]) {
     if constexpr (VEC) {
       if constexpr (IL) {
         sfor<0, 2>([&](auto PY_) {
           constexpr int py = decltype(PY_)::value;
-          const float* p = base[0] + off + (py ? half_pitch : 0ll);
+          const float* p = rowp[0] + (py ? half : 0ll);
           sfor<0, CW / 2>([&](auto Q_) {
             constexpr int q = decltype(Q_)::value;
             const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
@@ -274,7 +283,7 @@ struct RowReader {
       } else {
         sfor<0, 4>([&](auto J_) {
           constexpr int j = decltype(J_)::value;
-          const float* p = base[j] + row_off(j);
+          const float* p = rowp[j];
           if constexpr (CW == 4) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(p));
             d[j][0] = v.x, d[j][1] = v.y, d[j][2] = v.z, d[j][3] = v.w;
@@ -292,13 +301,13 @@ struct RowReader {
         sfor<0, 4>([&](auto J_) {
           constexpr int j = decltype(J_)::value;
           if constexpr (IL)
-            d[j][c] = __ldg(base[0] + off + ((j >> 1) ? half_pitch : 0ll) + 2 * xs[c] + (j & 1));
+            d[j][c] = __ldg(rowp[0] + ((j >> 1) ? half : 0ll) + 2 * xs[c] + (j & 1));
           else
-            d[j][c] = __ldg(base[j] + row_off(j) + xs[c]);
+            d[j][c] = __ldg(rowp[j] + xs[c]);
         });
       });
     }
-    advance();
+    advance(a);
   }
 };
 
@@ -404,7 +413,6 @@ level_kernel(const LevelArgs a) {
   const int rows = (y1 - y0) + M::U + M::L;
   const int iters = (rows + UNR - 1) / UNR * UNR;
   bool out_lane = lane >= 1 && lane <= kOutLanes;
-  const long long half_pitch = IN_IL ? a.in_pitch[0] : 0;
 
   float ring[S + 1][D][4][CW];
   sfor<1, S + 1>([&](auto B_) {
@@ -425,7 +433,7 @@ level_kernel(const LevelArgs a) {
   // prologue: rows n0 .. n0+PF-1 land in the slots iteration 0.. expect
   sfor<0, PF>([&](auto U_) {
     constexpr int u = decltype(U_)::value;
-    rd.load(ring[0][SC::slot(0, u, 0)], half_pitch);
+    rd.load(a, ring[0][SC::slot(0, u, 0)]);
   });
 
   for (int it = 0; it < iters; it += UNR) {
@@ -449,7 +457,7 @@ level_kernel(const LevelArgs a) {
       }
       eval_step<P, PF, 0, u, D, CW>(ring);
       // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
-      if (i + PF < rows) rd.load(ring[0][SC::slot(0, u, -PF)], half_pitch);
+      if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
       sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW>(ring); });
       const int y = n0 + i - M::L;
       if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);

@@ -36,6 +36,16 @@ struct LevelArgs {
   int nchunks;          // ceil(h2 / chunk_rows)
   int chunk_rows;
   int vec;              // 1: vector fast path valid (w2 % CW == 0, 16 B aligned)
+  // Row strips (multi-GPU): when halo != 0, component rows above the strip
+  // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from
+  // halo_bot (row y - h2) instead of wrapping periodically inside the strip.
+  // Same layout as `in` (interleaved: two image rows per component row).
+  int halo;
+  int up, down;         // halo rows available above / below (component rows)
+  const float* halo_top[4];
+  long long halo_top_pitch[4];
+  const float* halo_bot[4];
+  long long halo_bot_pitch[4];
 };
 
 using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);

@@ -135,6 +135,9 @@ void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t s
     if (!in_il || j == 0) {
       const size_t al = in_il ? 16 : size_t(4 * cw);
       vec = vec && aligned(a.in[j], al) && (a.in_pitch[j] * 4) % al == 0;
+      if (a.halo)
+        vec = vec && aligned(a.halo_top[j], al) && aligned(a.halo_bot[j], al) &&
+              (a.halo_top_pitch[j] * 4) % al == 0 && (a.halo_bot_pitch[j] * 4) % al == 0;
     }
     if (!out_il || j == 0) {
       const size_t al = out_il ? 16 : size_t(4 * cw);
@@ -468,6 +471,51 @@ int dwt2d_inverse_level(const dwt2d_plan* p, const float* const in[4], const siz
       a.in[j] = in[j], a.in_pitch[j] = (long long)in_pitch[j];
       a.out[j] = image, a.out_pitch[j] = (long long)pitch;
     }
+    a.w2 = width / 2, a.h2 = height / 2;
+    launch(*p, a, kToImage, as_stream(stream));
+  });
+}
+
+int dwt2d_forward_level_strip(const dwt2d_plan* p, const float* image, size_t pitch, int width, int height,
+                              const float* top, const float* bottom, size_t halo_pitch, float* const out[4],
+                              const size_t out_pitch[4], void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out || !out_pitch || !top || !bottom) fail(DWT2D_EINVAL, "null argument");
+    if (width <= 0 || height <= 0 || width % 2 || height % 2)
+      fail(DWT2D_EINVAL, "forward_level_strip: strip sides must be positive and even");
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    gpu::LevelArgs a{};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = image, a.in_pitch[j] = (long long)pitch;
+      a.halo_top[j] = top, a.halo_bot[j] = bottom;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)halo_pitch;
+      a.out[j] = out[j], a.out_pitch[j] = (long long)out_pitch[j];
+    }
+    a.halo = 1, a.up = p->up, a.down = p->down;
+    a.w2 = width / 2, a.h2 = height / 2;
+    launch(*p, a, kFromImage, as_stream(stream));
+  });
+}
+
+int dwt2d_inverse_level_strip(const dwt2d_plan* p, const float* const in[4], const size_t in_pitch[4],
+                              const float* const top[4], const float* const bottom[4],
+                              const size_t halo_pitch[4], float* image, size_t pitch, int width, int height,
+                              void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !in || !in_pitch || !top || !bottom || !halo_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (width <= 0 || height <= 0 || width % 2 || height % 2)
+      fail(DWT2D_EINVAL, "inverse_level_strip: strip sides must be positive and even");
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    gpu::LevelArgs a{};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = in[j], a.in_pitch[j] = (long long)in_pitch[j];
+      a.halo_top[j] = top[j], a.halo_bot[j] = bottom[j];
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)halo_pitch[j];
+      a.out[j] = image, a.out_pitch[j] = (long long)pitch;
+    }
+    a.halo = 1, a.up = p->up, a.down = p->down;
     a.w2 = width / 2, a.h2 = height / 2;
     launch(*p, a, kToImage, as_stream(stream));
   });

@@ -84,6 +84,10 @@ _SIGS = {
     "dwt2d_run_planar": (ctypes.c_int, [_p, _P4, _S4, _P4, _S4, ctypes.c_int, ctypes.c_int, _p]),
     "dwt2d_forward_level": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, _P4, _S4, _p]),
     "dwt2d_inverse_level": (ctypes.c_int, [_p, _P4, _S4, _p, _sz, ctypes.c_int, ctypes.c_int, _p]),
+    "dwt2d_forward_level_strip": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, _p, _p, _sz, _P4,
+                                                 _S4, _p]),
+    "dwt2d_inverse_level_strip": (ctypes.c_int, [_p, _P4, _S4, _P4, _P4, _S4, _p, _sz, ctypes.c_int,
+                                                 ctypes.c_int, _p]),
     "dwt2d_workspace_bytes": (_sz, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),

@@ -1,0 +1,128 @@
+"""Row-strip sharding of the Mallat pyramid across GPUs.
+
+A W x (N*H) image is split into N row strips, one per rank. Level l of the
+pyramid on rank r needs, besides its own strip of LL_{l-1}, the 2*up image
+rows directly above the strip (the previous rank's last rows) and the
+2*down rows directly below (the next rank's first rows); periodic extension
+closes the ring (rank N-1 <-> rank 0). `up`/`down` are the plan's component
+-row reach (2 and 2 for CDF 9/7: 4 image rows, 256 KiB per side at W=16384).
+
+Per level:  exchange halo rows with both ring neighbours (one batched
+send/recv round: NCCL over NVLink between GPUs, gloo on CPU)  ->  run the
+level on the strip with the halos as row sources (dwt2d_forward_level_strip,
+the same fused kernel as the single-GPU path)  ->  the strip of LL_l is the
+next level's input. Output per rank is a "strip Mallat" buffer (the rank's
+rows of every band, in the Mallat quadrant layout of its strip);
+`assemble_mallat` puts N of them back into the global layout.
+
+The exchange is the only collective; the level math never crosses ranks.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+
+def ring_neighbours(rank: int, world: int) -> tuple[int, int]:
+    return (rank - 1) % world, (rank + 1) % world
+
+
+def check_strip(h: int, w: int, up: int, down: int) -> None:
+    if h % 2 or w % 2 or h <= 0 or w <= 0:
+        raise ValueError("strip sides must be positive and even")
+    if h < 2 * up or h < 2 * down:
+        raise ValueError(f"strip of {h} rows is thinner than its halo ({2 * up}/{2 * down} rows); "
+                         "use fewer ranks or levels")
+
+
+class HaloExchange:
+    """Ring halo exchange over torch.distributed (any backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def __call__(self, strip, top_rows: int, bottom_rows: int):
+        """Returns (top, bottom): the rows above and below `strip` in the
+        global (periodic) image."""
+        if self.world == 1:  # periodic wrap of the only strip
+            return strip[-top_rows:], strip[:bottom_rows]
+        import torch
+        dist = self.dist
+        prev, nxt = ring_neighbours(self.rank, self.world)
+        top = torch.empty((top_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        bottom = torch.empty((bottom_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        # Post order matters when prev == next (2 ranks): messages between one
+        # pair of ranks match in posting order, so sends go [to prev: my first
+        # rows, to next: my last rows] and receives [from next: bottom, from
+        # prev: top] — the k-th send of one rank meets the k-th receive of the
+        # other for any world size.
+        ops = [
+            dist.P2POp(dist.isend, strip[:bottom_rows].contiguous(), prev, self.group),
+            dist.P2POp(dist.isend, strip[-top_rows:].contiguous(), nxt, self.group),
+            dist.P2POp(dist.irecv, bottom, nxt, self.group),
+            dist.P2POp(dist.irecv, top, prev, self.group),
+        ]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return top, bottom
+
+
+LevelFn = Callable[[object, object, object], Sequence[object]]
+
+
+def forward_mallat_strips(level_fn: LevelFn, strip, levels: int, up: int, down: int,
+                          exchange: Callable, out=None):
+    """Strip-sharded forward pyramid. level_fn(strip, top, bottom) returns
+    the strip's four bands (LL, HL, LH, HH). Works on torch tensors (CPU or
+    CUDA). Returns the rank's strip-Mallat buffer."""
+    import torch
+    h0, w0 = strip.shape
+    if out is None:
+        out = torch.empty_like(strip)
+    cur = strip
+    for lvl in range(levels):
+        h, w = cur.shape
+        check_strip(h, w, up, down)
+        top, bottom = exchange(cur, 2 * up, 2 * down)
+        ll, hl, lh, hh = level_fn(cur, top, bottom)
+        h2, w2 = h // 2, w // 2
+        out[:h2, w2:w] = hl
+        out[h2:h, :w2] = lh
+        out[h2:h, w2:w] = hh
+        cur = ll
+        if lvl == levels - 1:
+            out[:h2, :w2] = ll
+    return out
+
+
+def assemble_mallat(strips: Sequence, levels: int):
+    """Global Mallat layout from the per-rank strip-Mallat buffers."""
+    import torch
+    n = len(strips)
+    hs, W = strips[0].shape
+    H = hs * n
+    g = torch.empty((H, W), dtype=strips[0].dtype)
+    w, h = W, H
+    for lvl in range(levels):
+        w2, h2 = w // 2, h // 2
+        hl2 = (hs >> lvl) // 2  # band rows per rank at this level
+        for r, s in enumerate(strips):
+            s = s.cpu()
+            hsl = hs >> lvl  # rank's level-input rows
+            g[r * hl2:(r + 1) * hl2, w2:w] = s[:hl2, w2:w]
+            g[h2 + r * hl2:h2 + (r + 1) * hl2, :w2] = s[hl2:hsl, :w2]
+            g[h2 + r * hl2:h2 + (r + 1) * hl2, w2:w] = s[hl2:hsl, w2:w]
+            if lvl == levels - 1:
+                g[r * hl2:(r + 1) * hl2, :w2] = s[:hl2, :w2]
+        w, h = w2, h2
+    return g
+
+
+def gpu_level_fn(plan, stream=None) -> LevelFn:
+    """The product's level function: the fused sm_100a kernel with halo rows."""
+    def fn(cur, top, bottom):
+        return plan.forward_level_strip(cur, top, bottom, stream=stream)
+    return fn

@@ -134,6 +134,40 @@ class Plan:
                                           _stream_handle(stream)))
         return image
 
+    def forward_level_strip(self, strip, top, bottom, out: Sequence | None = None, stream=None):
+        """One forward level of a row strip; `top`/`bottom` are the 2*reach_up /
+        2*reach_down image rows above/below it (same width, common pitch)."""
+        import torch
+        H, W = strip.shape
+        if out is None:
+            out = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=strip.device) for _ in range(4)]
+        ptr, pitch = _dev(strip, "strip")
+        tptr, tpitch = _dev(top, "top")
+        bptr, bpitch = _dev(bottom, "bottom")
+        if tpitch != bpitch:
+            raise ValueError("top and bottom halos must share a pitch")
+        optr, opit = zip(*[_dev(o, "out") for o in out])
+        N.check(N.lib.dwt2d_forward_level_strip(self._h, ptr, pitch, W, H, tptr, bptr, tpitch,
+                                                N._P4(*optr), N._S4(*opit), _stream_handle(stream)))
+        return list(out)
+
+    def inverse_level_strip(self, planes: Sequence, tops: Sequence, bottoms: Sequence, image=None,
+                            stream=None):
+        import torch
+        h2, w2 = planes[0].shape
+        if image is None:
+            image = torch.empty((2 * h2, 2 * w2), dtype=torch.float32, device=planes[0].device)
+        iptr, ipit = zip(*[_dev(p, "plane") for p in planes])
+        tptr, tpit = zip(*[_dev(t, "top") for t in tops])
+        bptr, bpit = zip(*[_dev(b, "bottom") for b in bottoms])
+        if tuple(tpit) != tuple(bpit):
+            raise ValueError("top and bottom halos must share pitches")
+        ptr, pitch = _dev(image, "image")
+        N.check(N.lib.dwt2d_inverse_level_strip(self._h, N._P4(*iptr), N._S4(*ipit), N._P4(*tptr),
+                                                N._P4(*bptr), N._S4(*tpit), ptr, pitch, 2 * w2, 2 * h2,
+                                                _stream_handle(stream)))
+        return image
+
     def forward_mallat(self, image, levels: int, out=None, scratch=None, stream=None):
         import torch
         H, W = image.shape

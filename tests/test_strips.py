@@ -1,0 +1,151 @@
+"""Row-strip sharding: the multi-rank host logic on CPU with
+gloo (world sizes 2 and 3), and the device halo path on one GPU with
+virtual ranks (threads exchanging rows), both against the unsharded result.
+"""
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import dwt_oracle as O
+from paper_1704_08657_b200 import strips as S
+
+
+def oracle_level_fn(wavelet, scheme, opt, up, down):
+    """Level of the float64 oracle on [top; strip; bottom] cropped to the
+    strip's component rows (the periodic wrap of the tall image never reaches
+    them: every output row depends on rows up..down around it)."""
+    def fn(cur, top, bottom):
+        tall = torch.cat([top, cur, bottom]).double().numpy()
+        res = O.transform(wavelet, scheme, O.split(tall), opt)
+        h2 = cur.shape[0] // 2
+        return [torch.from_numpy(np.ascontiguousarray(r[up:up + h2])) for r in res]
+    return fn
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, args, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wavelet, scheme, opt, W, Hs, levels = args
+        img = O.random_image(W, Hs * world, 1, np.float64)
+        strip = torch.from_numpy(img[rank * Hs:(rank + 1) * Hs].copy())
+        out = S.forward_mallat_strips(oracle_level_fn(wavelet, scheme, opt, 2 if wavelet == "cdf97" else 1,
+                                                      2 if wavelet == "cdf97" else 1),
+                                      strip, levels, 2 if wavelet == "cdf97" else 1,
+                                      2 if wavelet == "cdf97" else 1, S.HaloExchange())
+        gathered = [torch.empty_like(out) for _ in range(world)]
+        dist.all_gather(gathered, out)
+        if rank == 0:
+            g = S.assemble_mallat(gathered, levels)
+            truth = O.pyramid(wavelet, scheme, img, levels, opt)
+            q.put(float(np.max(np.abs(g.numpy() - truth))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
+                                                ("cdf53", "separable-lifting", False)])
+def test_gloo_strip_pyramid_equals_full_image(world, wavelet, scheme, opt):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    args = (wavelet, scheme, opt, 32, 32, 3)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) < 1e-12
+
+
+def test_single_rank_exchange_is_periodic_wrap():
+    img = O.random_image(32, 32, 5, np.float64)
+    out = S.forward_mallat_strips(oracle_level_fn("cdf97", "nonseparable-lifting", True, 2, 2),
+                                  torch.from_numpy(img.copy()), 3, 2, 2, S.HaloExchange())
+    truth = O.pyramid("cdf97", "nonseparable-lifting", img, 3, True)
+    assert np.max(np.abs(out.numpy() - truth)) < 1e-12
+
+
+def test_strip_validation_and_assembly():
+    with pytest.raises(ValueError):
+        S.check_strip(2, 8, 2, 2)  # thinner than its 4-row halo
+    with pytest.raises(ValueError):
+        S.check_strip(6, 7, 1, 1)
+    assert S.ring_neighbours(0, 4) == (3, 1)
+    assert S.ring_neighbours(3, 4) == (2, 0)
+
+
+class VirtualRing:
+    """N ranks as threads in one process: each publishes its strip at every
+    level and reads its neighbours' rows (device tensors, same GPU)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.slots = [None] * world
+        self.barrier = threading.Barrier(world)
+
+    def exchange_for(self, rank):
+        def ex(strip, top_rows, bottom_rows):
+            self.slots[rank] = strip
+            self.barrier.wait()
+            prev, nxt = S.ring_neighbours(rank, self.world)
+            top = self.slots[prev][-top_rows:].contiguous()
+            bottom = self.slots[nxt][:bottom_rows].contiguous()
+            torch.cuda.synchronize()
+            self.barrier.wait()
+            return top, bottom
+        return ex
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
+                                                ("cdf97", "separable-convolution", False),
+                                                ("dd137", "nonseparable-lifting", True)])
+def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt):
+    """The halo-row path of the fused kernel reproduces the single-GPU
+    pyramid bit for bit (same arithmetic; halo rows are the same data)."""
+    import paper_1704_08657_b200 as dwt
+    plan = dwt.Plan(wavelet, scheme, optimized=opt)
+    up, down = plan.info["reach_up"], plan.info["reach_down"]
+    W, Hs, L = 256, 128, 4
+    img = torch.from_numpy(O.random_image(W, Hs * world, 3)).to(cuda)
+    full = plan.forward_mallat(img, L)
+    ring = VirtualRing(world)
+    outs = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(cuda)
+            strip = img[rank * Hs:(rank + 1) * Hs].contiguous()
+            outs[rank] = S.forward_mallat_strips(S.gpu_level_fn(plan), strip, L, up, down,
+                                                 ring.exchange_for(rank))
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            errors.append(e)
+            ring.barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    g = S.assemble_mallat(outs, L)
+    assert torch.equal(g, full.cpu())
