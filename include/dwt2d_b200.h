@@ -178,6 +178,18 @@ DWT2D_B200_API size_t dwt2d_workspace_bytes(int width, int height, int levels);
 DWT2D_B200_API int dwt2d_forward_mallat(const dwt2d_plan* plan, const float* image, size_t pitch,
                                         int width, int height, int levels, float* out,
                                         size_t out_pitch, void* scratch, void* stream);
+/* forward_mallat that also records CUDA events on `stream`: events[0] before
+ * level 1 and events[l] after level l (entries may be NULL; pass levels + 1
+ * entries). Inside stream capture the records become graph event-record
+ * nodes (cudaEventRecordExternal), so per-level kernel times can be read
+ * from a replayed graph. Events come from dwt2d_event_create. */
+DWT2D_B200_API int dwt2d_forward_mallat_ex(const dwt2d_plan* plan, const float* image, size_t pitch,
+                                           int width, int height, int levels, float* out,
+                                           size_t out_pitch, void* scratch, void* const* events,
+                                           void* stream);
+DWT2D_B200_API int dwt2d_event_create(void** event);
+DWT2D_B200_API int dwt2d_event_destroy(void* event);
+DWT2D_B200_API int dwt2d_event_elapsed_ms(void* start, void* end, float* ms);
 DWT2D_B200_API int dwt2d_inverse_mallat(const dwt2d_plan* inverse_plan, const float* in,
                                         size_t in_pitch, int width, int height, int levels,
                                         float* image, size_t pitch, void* scratch, void* stream);

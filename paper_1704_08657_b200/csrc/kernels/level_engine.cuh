@@ -405,7 +405,8 @@ level_kernel(const LevelArgs a) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  const int strip = wid % a.nstrips, chunk = wid / a.nstrips;
+  const int strip = wid % a.nstrips;
+  const int chunk = a.reverse ? a.nchunks - 1 - wid / a.nstrips : wid / a.nstrips;
   const int xc = (strip * kOutLanes - 1 + lane) * CW;  // first component column of this lane
   const int y0 = chunk * a.chunk_rows;
   const int y1 = min(a.h2, y0 + a.chunk_rows);

@@ -266,8 +266,18 @@ void get_workspace(Workspace& w, void* scratch, int W, int H, int levels, cudaSt
   w.owned = true;
 }
 
+void record(void* ev, cudaStream_t st) {
+  if (!ev) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cs), "capture status");
+  const unsigned flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, flags), "event record");
+}
+
 void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W, int H, int levels,
-                    float* out, size_t out_pitch, float* ws, cudaStream_t st) {
+                    float* out, size_t out_pitch, float* ws, cudaStream_t st,
+                    void* const* events = nullptr) {
+  if (events) record(events[0], st);
   const float* cur = image;
   size_t cur_pitch = pitch;
   for (int l = 1; l <= levels; ++l) {
@@ -284,7 +294,12 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     a.out[3] = out + size_t(h2) * out_pitch + w2;
     a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = (long long)out_pitch;
     a.w2 = w2, a.h2 = h2;
+    // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
+    // level l wrote last, which are still in L2 (LL uses normal stores, the
+    // detail bands evict-first).
+    a.reverse = (l % 2 == 0) ? 1 : 0;
     launch(p, a, kFromImage, st);
+    if (events) record(events[l], st);
     cur = ll;
     cur_pitch = ll_pitch;
   }
@@ -308,6 +323,7 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
     a.out[0] = a.out[1] = a.out[2] = a.out[3] = dst;
     for (int j = 0; j < 4; ++j) a.out_pitch[j] = (long long)dst_pitch;
     a.w2 = w2, a.h2 = h2;
+    a.reverse = ((levels - l) % 2 == 1) ? 1 : 0;
     if (!p.entry) fail(DWT2D_EUNSUPPORTED, "identity inverse pyramid");
     launch(p, a, kToImage, st);
     ll = dst;
@@ -539,6 +555,43 @@ int dwt2d_forward_mallat(const dwt2d_plan* p, const float* image, size_t pitch, 
     Workspace ws;
     get_workspace(ws, scratch, W, H, levels, as_stream(stream));
     forward_mallat(*p, image, pitch, W, H, levels, out, out_pitch, ws.ptr, as_stream(stream));
+  });
+}
+
+int dwt2d_forward_mallat_ex(const dwt2d_plan* p, const float* image, size_t pitch, int W, int H, int levels,
+                            float* out, size_t out_pitch, void* scratch, void* const* events, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
+    check_pyramid(W, H, levels);
+    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    Workspace ws;
+    get_workspace(ws, scratch, W, H, levels, as_stream(stream));
+    forward_mallat(*p, image, pitch, W, H, levels, out, out_pitch, ws.ptr, as_stream(stream), events);
+  });
+}
+
+int dwt2d_event_create(void** ev) {
+  return guard([&] {
+    if (!ev) fail(DWT2D_EINVAL, "null argument");
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "event create");
+    *ev = e;
+  });
+}
+
+int dwt2d_event_destroy(void* ev) {
+  return guard([&] {
+    if (ev) cuda_check(cudaEventDestroy(static_cast<cudaEvent_t>(ev)), "event destroy");
+  });
+}
+
+int dwt2d_event_elapsed_ms(void* a, void* b, float* ms) {
+  return guard([&] {
+    if (!a || !b || !ms) fail(DWT2D_EINVAL, "null argument");
+    cuda_check(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)),
+               "event elapsed");
   });
 }
 

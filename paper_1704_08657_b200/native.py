@@ -91,6 +91,11 @@ _SIGS = {
     "dwt2d_workspace_bytes": (_sz, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),
+    "dwt2d_forward_mallat_ex": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
+                                               _p, ctypes.POINTER(ctypes.c_void_p), _p]),
+    "dwt2d_event_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),
+    "dwt2d_event_destroy": (ctypes.c_int, [_p]),
+    "dwt2d_event_elapsed_ms": (ctypes.c_int, [_p, _p, ctypes.POINTER(ctypes.c_float)]),
     "dwt2d_inverse_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),
     "dwt2d_run_planar_host": (ctypes.c_int, [_p, _P4, _P4, ctypes.c_int, ctypes.c_int]),
@@ -122,6 +127,25 @@ def check(rc: int) -> None:
         if rc == EINVAL:
             raise ValueError(msg)
         raise DwtError(rc, msg)
+
+
+class Event:
+    """A CUDA timing event owned by the library (for dwt2d_forward_mallat_ex)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        check(lib.dwt2d_event_create(ctypes.byref(h)))
+        self.handle = h
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = ctypes.c_float()
+        check(lib.dwt2d_event_elapsed_ms(self.handle, end.handle, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None) and lib is not None:
+            lib.dwt2d_event_destroy(self.handle)
+            self.handle = None
 
 
 def registry_keys() -> list[str]:

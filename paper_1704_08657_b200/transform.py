@@ -168,16 +168,25 @@ class Plan:
                                                 _stream_handle(stream)))
         return image
 
-    def forward_mallat(self, image, levels: int, out=None, scratch=None, stream=None):
+    def forward_mallat(self, image, levels: int, out=None, scratch=None, stream=None, events=None):
+        """Mallat pyramid. events: optional list of levels + 1 native.Event (or
+        None entries) recorded before level 1 and after each level."""
         import torch
         H, W = image.shape
         if out is None:
             out = torch.empty((H, W), dtype=torch.float32, device=image.device)
         ptr, pitch = _dev(image, "image")
         optr, opitch = _dev(out, "out")
-        N.check(N.lib.dwt2d_forward_mallat(self._h, ptr, pitch, W, H, levels, optr, opitch,
-                                           None if scratch is None else scratch.data_ptr(),
-                                           _stream_handle(stream)))
+        scr = None if scratch is None else scratch.data_ptr()
+        if events is None:
+            N.check(N.lib.dwt2d_forward_mallat(self._h, ptr, pitch, W, H, levels, optr, opitch, scr,
+                                               _stream_handle(stream)))
+        else:
+            if len(events) != levels + 1:
+                raise ValueError("events needs levels + 1 entries")
+            arr = (ctypes.c_void_p * (levels + 1))(*[None if e is None else e.handle for e in events])
+            N.check(N.lib.dwt2d_forward_mallat_ex(self._h, ptr, pitch, W, H, levels, optr, opitch, scr, arr,
+                                                  _stream_handle(stream)))
         return out
 
     def inverse_mallat(self, coeffs, levels: int, image=None, scratch=None, stream=None):
