@@ -331,6 +331,143 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
   }
 }
 
+
+// ------------------------------------------------- host end-to-end pipeline
+//
+// Host image -> Mallat pyramid -> host, with the transfers overlapped with
+// level 1 (which streams by rows): the image goes up in row bands on an H2D
+// stream; level 1 of band b runs as a strip kernel whose halo rows are the
+// neighbouring bands' rows already on the device (the image's last rows are
+// uploaded first, for band 0's periodic top halo) as soon as band b + 1 has
+// landed; the band's three detail blocks go back on a D2H stream while later
+// bands are still uploading. Levels 2..L then run on the device-resident LL1
+// and only the top-left quadrant remains to be copied back.
+struct HostPipe {
+  cudaStream_t up = nullptr, comp = nullptr, down = nullptr;
+  std::vector<cudaEvent_t> ev;
+  void* buf = nullptr;  // grow-only device staging (mapping GBs per call costs tens of ms)
+  size_t cap = 0;
+  void* reserve(size_t bytes) {
+    if (bytes > cap) {
+      if (buf) cuda_check(cudaFree(buf), "free");
+      buf = nullptr;
+      cap = 0;
+      cuda_check(cudaMalloc(&buf, bytes), "device allocation");
+      cap = bytes;
+    }
+    return buf;
+  }
+  HostPipe() {
+    cuda_check(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking), "stream");
+  }
+  cudaEvent_t event(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+};
+
+HostPipe& host_pipe() {
+  static thread_local HostPipe pipe;
+  return pipe;
+}
+
+int band_rows_for(int H, int halo_rows) {
+  if (const char* env = std::getenv("DWT2D_HOST_BAND_ROWS")) {
+    const int v = std::atoi(env);
+    if (v > 0 && v % 2 == 0) return std::min(v, H);
+  }
+  int r = ((H / 16) + 1) & ~1;  // ~16 bands
+  r = std::max(r, std::max(64, 2 * halo_rows));
+  return std::min(r, H);
+}
+
+void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int W, int H, int levels,
+                                   float* out) {
+  HostPipe& hp = host_pipe();
+  const size_t n = size_t(W) * H, q = size_t(W / 2) * (H / 2);
+  const int top_rows = 2 * p.up, bot_rows = 2 * p.down;
+  if (top_rows > H || bot_rows > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
+  const size_t sub_ws = levels > 1 ? dwt2d_workspace_bytes(W / 2, H / 2, levels - 1) : 0;
+  const size_t bytes = (2 * n + q) * 4 + sub_ws + 256;
+  void* mem = hp.reserve(bytes);
+  float* d_img = static_cast<float*>(mem);
+  float* d_out = d_img + n;
+  float* d_ll1 = d_out + n;
+  float* d_sub = d_ll1 + ((q + 63) & ~size_t(63));
+  cudaEvent_t ev_alloc = hp.event(0);
+  cuda_check(cudaEventRecord(ev_alloc, hp.comp), "record");
+  cuda_check(cudaStreamWaitEvent(hp.up, ev_alloc), "wait");
+  cuda_check(cudaStreamWaitEvent(hp.down, ev_alloc), "wait");
+
+  const int R = band_rows_for(H, std::max(top_rows, bot_rows));
+  const int B = (H + R - 1) / R;
+  // the image's last rows first: band 0's (periodic) top halo
+  const size_t tail0 = size_t(H - top_rows) * W;
+  cuda_check(cudaMemcpyAsync(d_img + tail0, image + tail0, size_t(top_rows) * W * 4, cudaMemcpyHostToDevice,
+                             hp.up),
+             "H2D");
+  for (int b = 0; b < B; ++b) {
+    const int r0 = b * R, r1 = std::min(H, r0 + R);
+    const int c1 = (b == B - 1) ? std::max(r0, H - top_rows) : r1;  // tail rows already uploaded
+    if (c1 > r0)
+      cuda_check(cudaMemcpyAsync(d_img + size_t(r0) * W, image + size_t(r0) * W, size_t(c1 - r0) * W * 4,
+                                 cudaMemcpyHostToDevice, hp.up),
+                 "H2D");
+    cuda_check(cudaEventRecord(hp.event(1 + b), hp.up), "record");
+  }
+  const int w2 = W / 2, h2 = H / 2;
+  for (int b = 0; b < B; ++b) {
+    const int r0 = b * R, r1 = std::min(H, r0 + R);
+    // band b needs its own rows and the first rows of band b + 1 (its bottom halo)
+    cuda_check(cudaStreamWaitEvent(hp.comp, hp.event(1 + std::min(b + 1, B - 1))), "wait");
+    gpu::LevelArgs a{};
+    const float* top = r0 >= top_rows ? d_img + size_t(r0 - top_rows) * W : d_img + tail0;
+    const float* bot = r1 + bot_rows <= H ? d_img + size_t(r1) * W : d_img;
+    if (r0 < top_rows && r0 > 0) fail(DWT2D_EINVAL, "band rows smaller than the halo");
+    const int y0 = r0 / 2, hb = (r1 - r0) / 2;
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = d_img + size_t(r0) * W, a.in_pitch[j] = W;
+      a.halo_top[j] = top, a.halo_bot[j] = bot;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = W;
+    }
+    a.out[0] = (levels == 1 ? d_out + size_t(y0) * W : d_ll1 + size_t(y0) * w2);
+    a.out_pitch[0] = levels == 1 ? W : w2;
+    a.out[1] = d_out + size_t(y0) * W + w2;
+    a.out[2] = d_out + size_t(h2 + y0) * W;
+    a.out[3] = d_out + size_t(h2 + y0) * W + w2;
+    a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = W;
+    a.halo = 1, a.up = p.up, a.down = p.down;
+    a.w2 = w2, a.h2 = hb;
+    launch(p, a, kFromImage, hp.comp);
+    cudaEvent_t done = hp.event(1 + B + b);
+    cuda_check(cudaEventRecord(done, hp.comp), "record");
+    cuda_check(cudaStreamWaitEvent(hp.down, done), "wait");
+    // the band's rows of HL, LH, HH
+    const size_t pitch = size_t(W) * 4;
+    cuda_check(cudaMemcpy2DAsync(out + size_t(y0) * W + w2, pitch, d_out + size_t(y0) * W + w2, pitch,
+                                 size_t(w2) * 4, hb, cudaMemcpyDeviceToHost, hp.down),
+               "D2H");
+    cuda_check(cudaMemcpy2DAsync(out + size_t(h2 + y0) * W, pitch, d_out + size_t(h2 + y0) * W, pitch,
+                                 size_t(W) * 4, hb, cudaMemcpyDeviceToHost, hp.down),
+               "D2H");
+  }
+  if (levels > 1)
+    forward_mallat(p, d_ll1, size_t(w2), w2, h2, levels - 1, d_out, size_t(W), d_sub, hp.comp);
+  cudaEvent_t fin = hp.event(1 + 2 * B);
+  cuda_check(cudaEventRecord(fin, hp.comp), "record");
+  cuda_check(cudaStreamWaitEvent(hp.down, fin), "wait");
+  cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(w2) * 4, h2,
+                               cudaMemcpyDeviceToHost, hp.down),
+             "D2H");
+  cuda_check(cudaStreamSynchronize(hp.down), "synchronize");
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI
@@ -613,10 +750,9 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
     require_plan(p);
     if (!in || !out) fail(DWT2D_EINVAL, "null argument");
     if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    HostPipe& hp = host_pipe();
     const size_t n = size_t(w2) * h2;
-    float* dev = nullptr;
-    cuda_check(cudaMalloc(&dev, 8 * n * sizeof(float)), "device allocation");
-    std::unique_ptr<float, decltype(&cudaFree)> hold(dev, &cudaFree);
+    float* dev = static_cast<float*>(hp.reserve(8 * n * sizeof(float)));
     const float* din[4];
     float* dout[4];
     size_t pitch[4];
@@ -624,10 +760,10 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
       din[j] = dev + j * n;
       dout[j] = dev + (4 + j) * n;
       pitch[j] = size_t(w2);
-      cuda_check(cudaMemcpy(dev + j * n, in[j], n * 4, cudaMemcpyHostToDevice), "H2D");
+      cuda_check(cudaMemcpyAsync(dev + j * n, in[j], n * 4, cudaMemcpyHostToDevice, hp.comp), "H2D");
     }
     if (!p->entry) {
-      copy_planes(din, pitch, dout, pitch, w2, h2, nullptr);
+      copy_planes(din, pitch, dout, pitch, w2, h2, hp.comp);
     } else {
       gpu::LevelArgs a{};
       for (int j = 0; j < 4; ++j) {
@@ -635,10 +771,11 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
         a.in_pitch[j] = a.out_pitch[j] = w2;
       }
       a.w2 = w2, a.h2 = h2;
-      launch(*p, a, kPlanar, nullptr);
+      launch(*p, a, kPlanar, hp.comp);
     }
     for (int j = 0; j < 4; ++j)
-      cuda_check(cudaMemcpy(out[j], dout[j], n * 4, cudaMemcpyDeviceToHost), "D2H");
+      cuda_check(cudaMemcpyAsync(out[j], dout[j], n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
+    cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
   });
 }
 
@@ -649,20 +786,7 @@ int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, in
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
     if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
-    const size_t n = size_t(W) * H;
-    cudaStream_t st = nullptr;
-    void* d_img = nullptr;
-    void* d_out = nullptr;
-    cuda_check(cudaMallocAsync(&d_img, n * 4, st), "device allocation");
-    cuda_check(cudaMallocAsync(&d_out, n * 4, st), "device allocation");
-    Workspace ws;
-    get_workspace(ws, nullptr, W, H, levels, st);
-    cuda_check(cudaMemcpyAsync(d_img, image, n * 4, cudaMemcpyHostToDevice, st), "H2D");
-    forward_mallat(*p, static_cast<float*>(d_img), W, W, H, levels, static_cast<float*>(d_out), W, ws.ptr, st);
-    cuda_check(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    cudaFreeAsync(d_img, st);
-    cudaFreeAsync(d_out, st);
-    cuda_check(cudaStreamSynchronize(st), "synchronize");
+    forward_mallat_host_pipelined(*p, image, W, H, levels, out);
   });
 }
 
@@ -672,20 +796,16 @@ int dwt2d_inverse_mallat_host(const dwt2d_plan* p, const float* in, int W, int H
     if (!image || !in) fail(DWT2D_EINVAL, "null argument");
     if (p->forward) fail(DWT2D_EINVAL, "inverse_mallat: plan is not an inverse plan");
     check_pyramid(W, H, levels);
+    HostPipe& hp = host_pipe();
     const size_t n = size_t(W) * H;
-    cudaStream_t st = nullptr;
-    void* d_in = nullptr;
-    void* d_img = nullptr;
-    cuda_check(cudaMallocAsync(&d_in, n * 4, st), "device allocation");
-    cuda_check(cudaMallocAsync(&d_img, n * 4, st), "device allocation");
-    Workspace ws;
-    get_workspace(ws, nullptr, W, H, levels, st);
-    cuda_check(cudaMemcpyAsync(d_in, in, n * 4, cudaMemcpyHostToDevice, st), "H2D");
-    inverse_mallat(*p, static_cast<float*>(d_in), W, W, H, levels, static_cast<float*>(d_img), W, ws.ptr, st);
-    cuda_check(cudaMemcpyAsync(image, d_img, n * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    cudaFreeAsync(d_in, st);
-    cudaFreeAsync(d_img, st);
-    cuda_check(cudaStreamSynchronize(st), "synchronize");
+    const size_t ws_bytes = dwt2d_workspace_bytes(W, H, levels);
+    float* d_in = static_cast<float*>(hp.reserve(2 * n * 4 + ws_bytes + 256));
+    float* d_img = d_in + n;
+    float* ws = d_img + ((n + 63) & ~size_t(63));
+    cuda_check(cudaMemcpyAsync(d_in, in, n * 4, cudaMemcpyHostToDevice, hp.comp), "H2D");
+    inverse_mallat(*p, d_in, W, W, H, levels, d_img, W, ws, hp.comp);
+    cuda_check(cudaMemcpyAsync(image, d_img, n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
+    cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
   });
 }
 
