@@ -37,7 +37,8 @@ typedef enum {
   DWT2D_EINVAL = 1,      /* invalid argument (reference: std::invalid_argument) */
   DWT2D_ECUDA = 2,       /* CUDA runtime error */
   DWT2D_ENOMEM = 3,      /* device or host allocation failed */
-  DWT2D_EUNSUPPORTED = 4 /* no compiled kernel for this lowered program */
+  DWT2D_EUNSUPPORTED = 4 /* operation not available for this plan (e.g. row strips of a
+                            generic-executor plan) */
 } dwt2d_status;
 
 /* reference SchemeKind, scheme.hpp:13-20 (same order) */
@@ -107,6 +108,8 @@ typedef struct {
   int32_t forward;
   int32_t extension;
   int32_t fused_multiply_add;
+  int32_t generic;          /* 1: runs on the generic executor (one pass per sub-step:
+                               symmetric extension or no ahead-of-time kernel) */
 } dwt2d_plan_info;
 
 /* --- plans -------------------------------------------------------------- */

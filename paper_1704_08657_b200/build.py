@@ -100,6 +100,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
         units.append(("cxx", CSRC / s))
     for s in RUNTIME_SRCS:
         units.append(("cxx", CSRC / s))
+    units.append(("nvcc", CSRC / "kernels/generic_step.cu"))
     for cu in sorted((CSRC / "generated").glob("*.cu")):
         units.append(("nvcc", cu))
     objs = []

@@ -1,0 +1,76 @@
+// Generic GPU executor: one pass per lowered sub-step with the taps read from
+// a device table at run time — the reference's execution model
+// (proj/include/dwt2d/executor.hpp:146-238: one barrier-separated pass per
+// kernel, every tap through extend_index) on the GPU. It serves the programs
+// the fused AOT level kernels do not cover: symmetric extension (which
+// reflects every intermediate, incompatible with one streaming pass) and
+// definition-file wavelets of new shapes. Same accumulation order and
+// rounding as the fused kernels, so periodic results are bit-identical to
+// them and composed results to the reference's float32 executor.
+#include <cuda_runtime.h>
+
+#include "level_types.hpp"
+
+namespace dwt2d_b200 {
+namespace gpu {
+
+namespace {
+
+__device__ __forceinline__ int extend(int i, int n, int symmetric) {
+  if (i >= 0 && i < n) return i;
+  if (!symmetric) {
+    const int r = i % n;
+    return r < 0 ? r + n : r;
+  }
+  if (n == 1) return 0;
+  const int period = 2 * n - 2;
+  int r = i % period;
+  if (r < 0) r += period;
+  return r < n ? r : period - r;
+}
+
+__device__ __forceinline__ float load(const GenericStepArgs& a, int j, int x, int y) {
+  if (a.in_il) return a.in[0][(2ll * y + (j >> 1)) * a.in_pitch[0] + 2ll * x + (j & 1)];
+  return a.in[j][(long long)y * a.in_pitch[j] + x];
+}
+
+__global__ void __launch_bounds__(256) generic_step_kernel(const GenericStepArgs a) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= a.w2 || y >= a.h2) return;
+  for (int r = 0; r < 4; ++r) {
+    float v;
+    if (a.rows[r].ident) {
+      v = load(a, r, x, y);
+    } else {
+      float acc = 0.0f;
+      for (int t = a.rows[r].tb; t < a.rows[r].te; ++t) {
+        const TapDesc tp = a.taps[t];
+        const float s = load(a, tp.j, extend(x + tp.dm, a.w2, a.symmetric), extend(y + tp.dn, a.h2, a.symmetric));
+        if (t == a.rows[r].tb)
+          acc = tp.w == 1.0f ? s : __fmul_rn(tp.w, s);
+        else if (a.fma)
+          acc = __fmaf_rn(tp.w, s, acc);
+        else
+          acc = __fadd_rn(acc, tp.w == 1.0f ? s : __fmul_rn(tp.w, s));
+      }
+      v = a.rows[r].scale == 1.0f ? acc : __fmul_rn(acc, a.rows[r].scale);
+    }
+    if (a.out_il)
+      a.out[0][(2ll * y + (r >> 1)) * a.out_pitch[0] + 2ll * x + (r & 1)] = v;
+    else
+      a.out[r][(long long)y * a.out_pitch[r] + x] = v;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_generic_step(const GenericStepArgs& a, cudaStream_t st) {
+  const dim3 block(32, 8);
+  const dim3 grid((a.w2 + 31) / 32, (a.h2 + 7) / 8);
+  generic_step_kernel<<<grid, block, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace gpu
+}  // namespace dwt2d_b200

@@ -29,6 +29,7 @@
 // intermediates (executor.hpp:159-167) exactly.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -217,7 +218,25 @@ __device__ __forceinline__ int wrap(int i, int n) {
 // are fixed per lane; the row pointer advances by one pitch per row and is
 // recomputed only when the row crosses a segment boundary (no division in
 // the steady state).
-template <int CW, bool IL, bool VEC>
+template <bool COH>
+__device__ __forceinline__ float4 ld4(const float* p) {
+  if constexpr (COH) return __ldcg(reinterpret_cast<const float4*>(p));
+  else return __ldg(reinterpret_cast<const float4*>(p));
+}
+template <bool COH>
+__device__ __forceinline__ float2 ld2(const float* p) {
+  if constexpr (COH) return __ldcg(reinterpret_cast<const float2*>(p));
+  else return __ldg(reinterpret_cast<const float2*>(p));
+}
+template <bool COH>
+__device__ __forceinline__ float ld1(const float* p) {
+  if constexpr (COH) return __ldcg(p);
+  else return __ldg(p);
+}
+
+// COH: loads bypass the non-coherent path (needed when the input was written
+// earlier in the same launch, i.e. by a previous level of the tail kernel).
+template <int CW, bool IL, bool VEC, bool COH = false>
 struct RowReader {
   static constexpr int NP = IL ? 1 : 4;  // row pointers kept
   const float* rowp[NP];  // start of the current row (+ lane column for VEC)
@@ -273,7 +292,7 @@ struct RowReader {
           const float* p = rowp[0] + (py ? half : 0ll);
           sfor<0, CW / 2>([&](auto Q_) {
             constexpr int q = decltype(Q_)::value;
-            const float4 v = __ldg(reinterpret_cast<const float4*>(p) + q);
+            const float4 v = ld4<COH>(p + 4 * q);
             d[2 * py + 0][2 * q + 0] = v.x;
             d[2 * py + 1][2 * q + 0] = v.y;
             d[2 * py + 0][2 * q + 1] = v.z;
@@ -285,13 +304,13 @@ struct RowReader {
           constexpr int j = decltype(J_)::value;
           const float* p = rowp[j];
           if constexpr (CW == 4) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+            const float4 v = ld4<COH>(p);
             d[j][0] = v.x, d[j][1] = v.y, d[j][2] = v.z, d[j][3] = v.w;
           } else if constexpr (CW == 2) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+            const float2 v = ld2<COH>(p);
             d[j][0] = v.x, d[j][1] = v.y;
           } else {
-            sfor<0, CW>([&](auto C_) { d[j][decltype(C_)::value] = __ldg(p + decltype(C_)::value); });
+            sfor<0, CW>([&](auto C_) { d[j][decltype(C_)::value] = ld1<COH>(p + decltype(C_)::value); });
           }
         });
       }
@@ -301,9 +320,9 @@ struct RowReader {
         sfor<0, 4>([&](auto J_) {
           constexpr int j = decltype(J_)::value;
           if constexpr (IL)
-            d[j][c] = __ldg(rowp[0] + ((j >> 1) ? half : 0ll) + 2 * xs[c] + (j & 1));
+            d[j][c] = ld1<COH>(rowp[0] + ((j >> 1) ? half : 0ll) + 2 * xs[c] + (j & 1));
           else
-            d[j][c] = __ldg(rowp[j] + xs[c]);
+            d[j][c] = ld1<COH>(rowp[j] + xs[c]);
         });
       });
     }
@@ -396,15 +415,13 @@ struct RowWriter {
 
 // ------------------------------------------------------------- kernel
 
-template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
-level_kernel(const LevelArgs a) {
+// One work item: warp `wid` streams its (strip, chunk) of the level.
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH>
+__device__ __forceinline__ void level_item(const LevelArgs& a, const int wid) {
   using M = Meta<P>;
   using SC = Sched<P, PF>;
   constexpr int S = M::S, CW = M::CW, D = SC::D, UNR = SC::UNR, NS0 = SC::slots(0);
   const int lane = threadIdx.x & 31;
-  const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-  if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
   const int strip = wid % a.nstrips;
   const int chunk = a.reverse ? a.nchunks - 1 - wid / a.nstrips : wid / a.nstrips;
   const int xc = (strip * kOutLanes - 1 + lane) * CW;  // first component column of this lane
@@ -426,7 +443,7 @@ level_kernel(const LevelArgs a) {
     });
   });
 
-  RowReader<CW, IN_IL, VEC> rd;
+  RowReader<CW, IN_IL, VEC, COH> rd;
   rd.init(a, xc, n0);
   RowWriter<CW, OUT_IL, VEC> wr;
   wr.init(a, xc, n0 - M::L);
@@ -466,6 +483,38 @@ level_kernel(const LevelArgs a) {
     });
   }
   (void)NS0;
+}
+
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
+level_kernel(const LevelArgs a) {
+  const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
+  level_item<P, PF, IN_IL, OUT_IL, VEC, false>(a, wid);
+}
+
+// The deep, L2-resident levels of a pyramid in ONE cooperative launch: every
+// warp grid-strides over each level's work items, and a grid-wide barrier
+// separates consecutive levels (their LL feeds the next). Replaces a chain of
+// latency-bound launches whose per-level cost is a few microseconds of
+// launch and pipeline fill each. Loads use the coherent L2 path because the
+// inputs of levels 2.. are written inside this launch.
+template <class P, int PF, bool IN_IL, bool OUT_IL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+tail_kernel(const __grid_constant__ TailArgs t) {
+  const int gw = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kWarpsPerCta;
+  for (int l = 0; l < t.nlev; ++l) {
+    const LevelArgs& a = t.lv[l];
+    const int items = a.nstrips * a.nchunks;
+    for (int w = gw; w < items; w += nw) {  // warp-uniform trip count
+      if (a.vec)
+        level_item<P, PF, IN_IL, OUT_IL, true, true>(a, w);
+      else
+        level_item<P, PF, IN_IL, OUT_IL, false, true>(a, w);
+    }
+    if (l + 1 < t.nlev) cooperative_groups::this_grid().sync();
+  }
 }
 
 }  // namespace gpu

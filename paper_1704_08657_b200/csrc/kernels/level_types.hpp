@@ -50,6 +50,14 @@ struct LevelArgs {
 };
 
 using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
+
+constexpr int kMaxTailLevels = 12;
+struct TailArgs {
+  LevelArgs lv[kMaxTailLevels];
+  int nlev;
+};
+// cooperative launch of the fused deep-level kernel; grid = `blocks` CTAs
+using TailLaunch = cudaError_t (*)(const TailArgs&, int blocks, cudaStream_t);
 // resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
 using LevelOccupancy = int (*)();
 
@@ -63,7 +71,26 @@ struct PlanEntry {
   LevelLaunch from_image;      // interleaved -> 4 planes (forward levels)
   LevelLaunch to_image;        // 4 planes -> interleaved (inverse levels)
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
+  TailLaunch tail;             // fused deep levels (same direction as from_image/to_image)
+  LevelOccupancy tail_occupancy;
 };
+
+// One sub-step of the generic executor (kernels/generic_step.cu). `taps`
+// points to device memory owned by the plan.
+struct GenericStepArgs {
+  const float* in[4];
+  long long in_pitch[4];
+  int in_il;             // in[0] is an interleaved image
+  float* out[4];
+  long long out_pitch[4];
+  int out_il;            // out[0] is an interleaved image
+  int w2, h2;
+  int symmetric;         // extend_index rule on the component grid
+  int fma;               // rounding model (see lowering.hpp)
+  RowDesc rows[4];
+  const TapDesc* taps;
+};
+cudaError_t launch_generic_step(const GenericStepArgs& a, cudaStream_t st);
 
 const std::vector<PlanEntry>& plan_registry();
 const PlanEntry* find_plan(unsigned long long fingerprint);

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -36,6 +37,13 @@ struct dwt2d_plan {
   std::string description;
   std::vector<dwt2d_row> rows;
   std::vector<dwt2d_tap> taps;
+  // generic executor (symmetric extension, programs without an AOT kernel)
+  bool generic = false;
+  mutable std::once_flag dev_once;
+  mutable dwt2d_b200::gpu::TapDesc* d_taps = nullptr;
+  ~dwt2d_plan() {
+    if (d_taps) cudaFree(d_taps);
+  }
 };
 
 namespace {
@@ -122,12 +130,13 @@ int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
 
 enum Layout { kPlanar, kFromImage, kToImage };
 
-void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
+// Work decomposition and vector-path eligibility of one level launch.
+void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_override = 0) {
   if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
-  a.chunk_rows = chunk_rows_for(p, a.h2, a.nstrips);
+  a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, a.h2) : chunk_rows_for(p, a.h2, a.nstrips);
   a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
   bool vec = a.w2 % cw == 0;
   const bool in_il = layout == kFromImage, out_il = layout == kToImage;
@@ -145,6 +154,86 @@ void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t s
     }
   }
   a.vec = vec ? 1 : 0;
+}
+
+void keep_pool_memory() {
+  // stream-ordered allocations (workspaces, generic temporaries) are reused
+  // instead of being unmapped at every synchronisation
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  });
+}
+
+const gpu::TapDesc* device_taps(const dwt2d_plan& p) {
+  std::call_once(p.dev_once, [&] {
+    std::vector<gpu::TapDesc> t;
+    for (const dwt2d_tap& k : p.taps) t.push_back(gpu::TapDesc{k.comp, k.dm, k.dn, k.w});
+    if (t.empty()) t.push_back(gpu::TapDesc{0, 0, 0, 0.0f});
+    gpu::TapDesc* d = nullptr;
+    cuda_check(cudaMalloc(&d, t.size() * sizeof(gpu::TapDesc)), "tap table allocation");
+    cuda_check(cudaMemcpy(d, t.data(), t.size() * sizeof(gpu::TapDesc), cudaMemcpyHostToDevice), "tap table upload");
+    p.d_taps = d;
+  });
+  if (!p.d_taps) fail(DWT2D_ECUDA, "tap table unavailable");
+  return p.d_taps;
+}
+
+// One level on the generic executor: sub-step s reads the previous
+// sub-step's planes (double-buffered temporaries), like the reference's run().
+void run_generic(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+  if (a.halo) fail(DWT2D_EUNSUPPORTED, "row strips need a fused kernel (periodic built-in program)");
+  keep_pool_memory();
+  const gpu::TapDesc* taps = device_taps(p);
+  const int S = p.substeps;
+  const size_t plane = size_t(a.w2) * size_t(a.h2);
+  float* tmp = nullptr;
+  if (S > 1) {
+    void* m = nullptr;
+    cuda_check(cudaMallocAsync(&m, (S > 2 ? 8 : 4) * plane * sizeof(float), st), "generic temporaries");
+    tmp = static_cast<float*>(m);
+  }
+  for (int s = 0; s < S; ++s) {
+    gpu::GenericStepArgs g{};
+    const bool first = s == 0, last = s == S - 1;
+    float* src_tmp = tmp + size_t((s - 1) % 2) * 4 * plane;
+    float* dst_tmp = tmp + size_t(s % 2) * 4 * plane;
+    for (int j = 0; j < 4; ++j) {
+      g.in[j] = first ? a.in[j] : src_tmp + j * plane;
+      g.in_pitch[j] = first ? a.in_pitch[j] : a.w2;
+      g.out[j] = last ? a.out[j] : dst_tmp + j * plane;
+      g.out_pitch[j] = last ? a.out_pitch[j] : a.w2;
+      const dwt2d_row& r = p.rows[size_t(s) * 4 + j];
+      g.rows[j] = gpu::RowDesc{r.identity, r.tap_begin, r.tap_end, r.scale};
+    }
+    g.in_il = first && layout == kFromImage;
+    g.out_il = last && layout == kToImage;
+    g.w2 = a.w2, g.h2 = a.h2;
+    g.symmetric = p.extension == DWT2D_SYMMETRIC;
+    g.fma = p.fma;
+    g.taps = taps;
+    cuda_check(gpu::launch_generic_step(g, st), "generic step launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (tmp) cuda_check(cudaFreeAsync(tmp, st), "generic temporaries");
+}
+
+void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
+  if (p.generic) {
+    if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    if (layout != kPlanar && (layout == kToImage) == (p.forward != 0))
+      fail(DWT2D_EINVAL, layout == kToImage ? "inverse_level: plan is not an inverse plan"
+                                            : "forward_level: plan is an inverse plan");
+    return run_generic(p, a, layout, st);
+  }
+  prepare(p, a, layout);
+  const gpu::PlanEntry& e = *p.entry;
   gpu::LevelLaunch fn = layout == kPlanar ? e.planar : layout == kFromImage ? e.from_image : e.to_image;
   if (!fn)
     fail(DWT2D_EINVAL, layout == kToImage ? "inverse_level: plan is not an inverse plan"
@@ -152,6 +241,45 @@ void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t s
   cuda_check(fn(a, st), "level kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
+
+// Levels whose input is at most this many bytes run fused in one cooperative
+// tail launch (they are L2-resident and latency bound). DWT2D_TAIL_BYTES
+// overrides; 0 disables the tail.
+size_t tail_bytes() {
+  if (const char* env = std::getenv("DWT2D_TAIL_BYTES")) return size_t(std::atoll(env));
+  return 0;  // measured: no faster than per-level launches on B200
+}
+
+// Launches the levels in `lv` (already filled, consecutive, same direction)
+// as one cooperative kernel.
+void launch_tail(const dwt2d_plan& p, std::vector<gpu::LevelArgs>& lv, Layout layout, cudaStream_t st) {
+  const gpu::PlanEntry& e = *p.entry;
+  static thread_local const gpu::PlanEntry* cached = nullptr;
+  static thread_local int per_sm = 0;
+  if (cached != &e) {
+    cached = &e;
+    per_sm = e.tail_occupancy ? e.tail_occupancy() : 0;
+  }
+  if (per_sm <= 0) fail(DWT2D_ECUDA, "tail kernel cannot be resident");
+  const int blocks = per_sm * sm_count();
+  const long long warps = (long long)blocks * gpu::kWarpsPerCta;
+  gpu::TailArgs t{};
+  t.nlev = int(lv.size());
+  for (size_t i = 0; i < lv.size(); ++i) {
+    gpu::LevelArgs& a = lv[i];
+    const int cw = e.cw;
+    const int nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
+    // one pass of the grid's warps over the level's work items
+    const long long rows = (long long)a.h2 * nstrips;
+    const int chunk = int(std::max<long long>(2, (rows + warps - 1) / warps));
+    prepare(p, a, layout, chunk);
+    t.lv[i] = a;
+  }
+  cuda_check(e.tail(t, blocks, st), "tail kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+bool is_identity(const dwt2d_plan& p) { return !p.entry && !p.generic; }
 
 void require_plan(const dwt2d_plan* p) {
   if (!p) fail(DWT2D_EINVAL, "null plan");
@@ -181,12 +309,13 @@ void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) identity = identity && r.identity;
   if (identity) return;  // pure copy, no kernel (pairless wavelet)
-  if (extension != DWT2D_PERIODIC)
-    fail(DWT2D_EUNSUPPORTED, "symmetric extension has no compiled kernel yet (" + p.key + ")");
-  p.entry = gpu::find_plan(p.fingerprint);
-  if (!p.entry)
-    fail(DWT2D_EUNSUPPORTED, "no compiled level kernel for program " + p.key +
-                                 " (custom wavelets are not compiled ahead of time)");
+  // the fused single-pass kernels cover periodic extension of the built-in
+  // programs; everything else runs on the generic GPU executor (one pass per
+  // sub-step, kernels/generic_step.cu)
+  const char* force = std::getenv("DWT2D_FORCE_GENERIC");  // testing: bypass the fused kernels
+  const bool fused_ok = extension == DWT2D_PERIODIC && !(force && *force && *force != '0');
+  p.entry = fused_ok ? gpu::find_plan(p.fingerprint) : nullptr;
+  p.generic = p.entry == nullptr;
 }
 
 StepProgram program_from_tables(const dwt2d_program& t) {
@@ -280,6 +409,9 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
   if (events) record(events[0], st);
   const float* cur = image;
   size_t cur_pitch = pitch;
+  std::vector<gpu::LevelArgs> tail;
+  int tail_first = 0;
+  const size_t tail_limit = tail_bytes();
   for (int l = 1; l <= levels; ++l) {
     const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
     gpu::LevelArgs a{};
@@ -298,10 +430,22 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     // level l wrote last, which are still in L2 (LL uses normal stores, the
     // detail bands evict-first).
     a.reverse = (l % 2 == 0) ? 1 : 0;
-    launch(p, a, kFromImage, st);
-    if (events) record(events[l], st);
+    const bool small = p.entry && size_t(w) * size_t(h) * 4 <= tail_limit && levels - l + 1 >= 2 &&
+                       levels - l + 1 <= gpu::kMaxTailLevels;
+    if (!tail.empty() || small) {
+      if (tail.empty()) tail_first = l;
+      tail.push_back(a);
+    } else {
+      launch(p, a, kFromImage, st);
+      if (events) record(events[l], st);
+    }
     cur = ll;
     cur_pitch = ll_pitch;
+  }
+  if (!tail.empty()) {
+    launch_tail(p, tail, kFromImage, st);
+    if (events)
+      for (int l = tail_first; l <= levels; ++l) record(events[l], st);
   }
 }
 
@@ -309,6 +453,9 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
                     float* image, size_t pitch, float* ws, cudaStream_t st) {
   const float* ll = in;
   size_t ll_pitch = in_pitch;
+  if (is_identity(p)) fail(DWT2D_EUNSUPPORTED, "identity inverse pyramid");
+  std::vector<gpu::LevelArgs> tail;
+  const size_t tail_limit = tail_bytes();
   for (int l = levels; l >= 1; --l) {
     const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
     gpu::LevelArgs a{};
@@ -324,13 +471,25 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
     for (int j = 0; j < 4; ++j) a.out_pitch[j] = (long long)dst_pitch;
     a.w2 = w2, a.h2 = h2;
     a.reverse = ((levels - l) % 2 == 1) ? 1 : 0;
-    if (!p.entry) fail(DWT2D_EUNSUPPORTED, "identity inverse pyramid");
-    launch(p, a, kToImage, st);
+    // the deepest levels come first here: batch them while they stay small
+    const bool small = p.entry && size_t(w) * size_t(h) * 4 <= tail_limit &&
+                       int(tail.size()) < gpu::kMaxTailLevels;
+    if (small && l > 1) {
+      tail.push_back(a);
+    } else {
+      if (!tail.empty()) {
+        if (tail.size() == 1)
+          launch(p, tail[0], kToImage, st);
+        else
+          launch_tail(p, tail, kToImage, st);
+        tail.clear();
+      }
+      launch(p, a, kToImage, st);
+    }
     ll = dst;
     ll_pitch = dst_pitch;
   }
 }
-
 
 // ------------------------------------------------- host end-to-end pipeline
 //
@@ -546,6 +705,7 @@ int dwt2d_plan_get_info(const dwt2d_plan* p, dwt2d_plan_info* info) {
     info->forward = p->forward;
     info->extension = p->extension;
     info->fused_multiply_add = p->fma;
+    info->generic = p->generic ? 1 : 0;
   });
 }
 
@@ -580,7 +740,7 @@ int dwt2d_run_planar(const dwt2d_plan* p, const float* const in[4], const size_t
     require_plan(p);
     if (!in || !out || !in_pitch || !out_pitch) fail(DWT2D_EINVAL, "null argument");
     if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
-    if (!p->entry) return copy_planes(in, in_pitch, out, out_pitch, w2, h2, as_stream(stream));
+    if (is_identity(*p)) return copy_planes(in, in_pitch, out, out_pitch, w2, h2, as_stream(stream));
     gpu::LevelArgs a{};
     for (int j = 0; j < 4; ++j) {
       a.in[j] = in[j], a.out[j] = out[j];
@@ -600,7 +760,7 @@ int dwt2d_forward_level(const dwt2d_plan* p, const float* image, size_t pitch, i
     if (width <= 0 || height <= 0) fail(DWT2D_EINVAL, "polyphase_split: empty image");
     if (width % 2) fail(DWT2D_EINVAL, "polyphase_split: odd image width");
     if (height % 2) fail(DWT2D_EINVAL, "polyphase_split: odd image height");
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     gpu::LevelArgs a{};
     for (int j = 0; j < 4; ++j) {
       a.in[j] = image, a.in_pitch[j] = (long long)pitch;
@@ -618,7 +778,7 @@ int dwt2d_inverse_level(const dwt2d_plan* p, const float* const in[4], const siz
     if (!image || !in || !in_pitch) fail(DWT2D_EINVAL, "null argument");
     if (width <= 0 || height <= 0 || width % 2 || height % 2)
       fail(DWT2D_EINVAL, "inverse_level: image sides must be positive and even");
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     gpu::LevelArgs a{};
     for (int j = 0; j < 4; ++j) {
       a.in[j] = in[j], a.in_pitch[j] = (long long)in_pitch[j];
@@ -637,7 +797,7 @@ int dwt2d_forward_level_strip(const dwt2d_plan* p, const float* image, size_t pi
     if (!image || !out || !out_pitch || !top || !bottom) fail(DWT2D_EINVAL, "null argument");
     if (width <= 0 || height <= 0 || width % 2 || height % 2)
       fail(DWT2D_EINVAL, "forward_level_strip: strip sides must be positive and even");
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     gpu::LevelArgs a{};
     for (int j = 0; j < 4; ++j) {
       a.in[j] = image, a.in_pitch[j] = (long long)pitch;
@@ -660,7 +820,7 @@ int dwt2d_inverse_level_strip(const dwt2d_plan* p, const float* const in[4], con
     if (!image || !in || !in_pitch || !top || !bottom || !halo_pitch) fail(DWT2D_EINVAL, "null argument");
     if (width <= 0 || height <= 0 || width % 2 || height % 2)
       fail(DWT2D_EINVAL, "inverse_level_strip: strip sides must be positive and even");
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     gpu::LevelArgs a{};
     for (int j = 0; j < 4; ++j) {
       a.in[j] = in[j], a.in_pitch[j] = (long long)in_pitch[j];
@@ -688,7 +848,7 @@ int dwt2d_forward_mallat(const dwt2d_plan* p, const float* image, size_t pitch, 
     if (!image || !out) fail(DWT2D_EINVAL, "null argument");
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     Workspace ws;
     get_workspace(ws, scratch, W, H, levels, as_stream(stream));
     forward_mallat(*p, image, pitch, W, H, levels, out, out_pitch, ws.ptr, as_stream(stream));
@@ -702,7 +862,7 @@ int dwt2d_forward_mallat_ex(const dwt2d_plan* p, const float* image, size_t pitc
     if (!image || !out) fail(DWT2D_EINVAL, "null argument");
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
     Workspace ws;
     get_workspace(ws, scratch, W, H, levels, as_stream(stream));
     forward_mallat(*p, image, pitch, W, H, levels, out, out_pitch, ws.ptr, as_stream(stream), events);
@@ -762,7 +922,7 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
       pitch[j] = size_t(w2);
       cuda_check(cudaMemcpyAsync(dev + j * n, in[j], n * 4, cudaMemcpyHostToDevice, hp.comp), "H2D");
     }
-    if (!p->entry) {
+    if (is_identity(*p)) {
       copy_planes(din, pitch, dout, pitch, w2, h2, hp.comp);
     } else {
       gpu::LevelArgs a{};
@@ -785,8 +945,21 @@ int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, in
     if (!image || !out) fail(DWT2D_EINVAL, "null argument");
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
-    if (!p->entry) fail(DWT2D_EUNSUPPORTED, "identity program");
-    forward_mallat_host_pipelined(*p, image, W, H, levels, out);
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (p->entry) {
+      forward_mallat_host_pipelined(*p, image, W, H, levels, out);
+    } else {
+      HostPipe& hp = host_pipe();
+      const size_t n = size_t(W) * H;
+      const size_t ws_bytes = dwt2d_workspace_bytes(W, H, levels);
+      float* d_img = static_cast<float*>(hp.reserve(2 * n * 4 + ws_bytes + 256));
+      float* d_out = d_img + n;
+      float* ws = d_out + ((n + 63) & ~size_t(63));
+      cuda_check(cudaMemcpyAsync(d_img, image, n * 4, cudaMemcpyHostToDevice, hp.comp), "H2D");
+      forward_mallat(*p, d_img, W, W, H, levels, d_out, W, ws, hp.comp);
+      cuda_check(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
+      cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
+    }
   });
 }
 

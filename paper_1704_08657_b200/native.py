@@ -63,7 +63,8 @@ class PlanInfo(ctypes.Structure):
                 ("reach_left", ctypes.c_int32), ("reach_right", ctypes.c_int32),
                 ("reach_up", ctypes.c_int32), ("reach_down", ctypes.c_int32),
                 ("columns_per_lane", ctypes.c_int32), ("forward", ctypes.c_int32),
-                ("extension", ctypes.c_int32), ("fused_multiply_add", ctypes.c_int32)]
+                ("extension", ctypes.c_int32), ("fused_multiply_add", ctypes.c_int32),
+                ("generic", ctypes.c_int32)]
 
 
 _p = ctypes.c_void_p

@@ -76,11 +76,12 @@ int main(int argc, char** argv) {
   const size_t n = size_t(W / 2) * (H / 2);
   std::vector<float> ref(n), host(n);
   using P = plans::cdf97_nonseparable_lifting_opt;
-  run<WithCW<P, 4>, 2, 1>("base cw4", img, out, W, H, 64, nullptr, nullptr);
-  CK(cudaMemcpy(ref.data(), out[3], n * 4, cudaMemcpyDeviceToHost));
-  for (int sz : {16384, 8192, 4096}) {
-    for (int chunk : {8, 16, 24, 32, 48, 64, 96}) {
+  for (int sz : {2048, 1024, 512, 256, 128}) {
+    for (int chunk : {2, 4, 8}) {
       run<WithCW<P, 4>, 2, 1>("cw4 pf2", img, out, sz, sz, chunk, nullptr, nullptr);
+      run<WithCW<P, 2>, 4, 1>("cw2 pf4", img, out, sz, sz, chunk, nullptr, nullptr);
+      run<WithCW<P, 2>, 8, 1>("cw2 pf8", img, out, sz, sz, chunk, nullptr, nullptr);
+      run<WithCW<P, 4>, 8, 1>("cw4 pf8", img, out, sz, sz, chunk, nullptr, nullptr);
     }
   }
   // plain copy kernel for the same bytes as a sanity ceiling

@@ -183,6 +183,28 @@ def test_host_entry_points_match_device(dwt, cuda):
     assert float(np.max(np.abs(back - img))) <= 5e-5
 
 
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
+                                     ("dd137", "nonseparable-polyconvolution", False),
+                                     ("cdf97", "nonseparable-convolution", True)])
+def test_fused_tail_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+    """Deep levels fused into one cooperative launch give the same bits as
+    one launch per level, forward and inverse, incl. scalar-path levels."""
+    import torch
+    plan = dwt.Plan(w, s, optimized=opt)
+    inv = dwt.Plan(w, "inverse-lifting")
+    for W, H, L in [(512, 384, 7), (96, 64, 5)]:
+        img = torch.from_numpy(O.random_image(W, H, 8)).to(cuda)
+        monkeypatch.setenv("DWT2D_TAIL_BYTES", "0")
+        a = plan.forward_mallat(img, L)
+        ia = inv.inverse_mallat(a, L)
+        monkeypatch.setenv("DWT2D_TAIL_BYTES", str(1 << 30))
+        b = plan.forward_mallat(img, L)
+        ib = inv.inverse_mallat(a, L)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), (W, H, L)
+        assert torch.equal(ia, ib), (W, H, L)
+
+
 @pytest.mark.parametrize("band_rows", ["64", "96", "10000"])
 def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, monkeypatch):
     """The pipelined host entry point (row bands uploaded while level 1 runs
@@ -229,13 +251,116 @@ def test_validation_errors(dwt, cuda):
         dwt.Plan("cdf53", "separable-lifting", workers=0)
 
 
-def test_launch_count_and_native_library_loaded(dwt, cuda):
+def test_launch_count_and_native_library_loaded(dwt, cuda, monkeypatch):
     import torch
     from paper_1704_08657_b200 import native
-    before = dwt.launch_count()
     plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
-    plan.forward_mallat(torch.from_numpy(O.random_image(256, 256, 2)).to(cuda), 8)
+    img = torch.from_numpy(O.random_image(256, 256, 2)).to(cuda)
+    monkeypatch.setenv("DWT2D_TAIL_BYTES", "0")  # one launch per level
+    before = dwt.launch_count()
+    plan.forward_mallat(img, 8)
     torch.cuda.synchronize()
     assert dwt.launch_count() - before == 8
+    monkeypatch.setenv("DWT2D_TAIL_BYTES", str(64 << 20))  # all 8 levels fused
+    before = dwt.launch_count()
+    plan.forward_mallat(img, 8)
+    torch.cuda.synchronize()
+    assert dwt.launch_count() - before == 1
     maps = open("/proc/self/maps").read()
     assert str(native.LIB_PATH) in maps
+
+
+# ---------------------------------------------------------------- symmetric
+# extend_index's whole-sample symmetric rule applied to every intermediate of
+# every step (image.hpp:21-25, executor.hpp:159-167), on the generic
+# executor (one pass per sub-step).
+
+SYM_SIZES = [(32, 24), (17, 9), (2, 3), (1, 1)]
+
+
+@pytest.mark.parametrize("w,s,opt", PLANS)
+def test_symmetric_matches_float64_oracle(dwt, cuda, w, s, opt):
+    plan = dwt.Plan(w, s, optimized=opt, extension="symmetric")
+    scheme = O.make(w, s, opt)
+    for (w2, h2) in SYM_SIZES:
+        planes = O.split(O.random_image(2 * w2, 2 * h2, 31 + w2))
+        got = [t.cpu().numpy() for t in plan.run(_to_dev(planes, cuda))]
+        truth = O.run(scheme, planes, symmetric=True)
+        peak = max(float(np.max(np.abs(p))) for p in planes) or 1.0
+        assert _err(got, truth, peak) <= TOL, (w, s, opt, w2, h2)
+
+
+@pytest.mark.parametrize("w,s,opt", [p for p in PLANS if not p[2]])
+def test_symmetric_composed_bit_exact_vs_reference(dwt, cuda, w, s, opt):
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    plan = dwt.Plan(w, s, optimized=opt, extension="symmetric", lowering="composed")
+    for (w2, h2) in [(32, 24), (17, 9), (2, 3)]:
+        planes = O.split(O.random_image(2 * w2, 2 * h2, 5 + h2))
+        got = [t.cpu().numpy() for t in plan.run(_to_dev(planes, cuda))]
+        ref, _ = R.run(w, s, planes, optimized=opt, symmetric=True)
+        for j in range(4):
+            assert np.array_equal(got[j], ref[j]), (w, s, w2, h2, j)
+
+
+@pytest.mark.parametrize("w", WAVELETS)
+def test_symmetric_reconstruction(dwt, cuda, w):
+    """test_executor.cpp:300-326: with symmetric extension the lifting schemes
+    reconstruct everywhere, the convolution family on the interior."""
+    inv = dwt.Plan(w, "inverse-lifting", extension="symmetric")
+    planes = _to_dev(O.split(O.random_image(64, 48, 404)), cuda)
+    for s in FORWARD:
+        back = inv.run(dwt.Plan(w, s, extension="symmetric").run(planes))
+        margin = 0 if "lifting" in s else 8
+        sl = (slice(margin, -margin or None), slice(margin, -margin or None))
+        e = max(float((b[sl] - p[sl]).abs().max()) for b, p in zip(back, planes))
+        assert e <= 5e-5 * (8 if w == "dd137" else 1), (s, e)
+
+
+def test_symmetric_pyramid_and_inverse(dwt, cuda):
+    import torch
+    W, H, L = 128, 96, 4
+    img = O.random_image(W, H, 2)
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+    got = plan.forward_mallat(torch.from_numpy(img).to(cuda), L)
+    truth = O.pyramid("cdf97", "nonseparable-lifting", img, L, True, symmetric=True)
+    assert max(O.level_errors(got.cpu().numpy(), truth, img, L)) <= TOL
+    inv = dwt.Plan("cdf97", "inverse-lifting", extension="symmetric")
+    back = inv.inverse_mallat(got, L)
+    assert float((back.cpu() - torch.from_numpy(img)).abs().max()) <= 5e-5
+
+
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-convolution", False),
+                                     ("dd137", "inverse-lifting", False)])
+def test_generic_executor_equals_fused_kernels(dwt, cuda, w, s, opt, monkeypatch):
+    """Same tables, same order, same rounding: the generic per-sub-step
+    executor and the fused single-pass kernel agree bit for bit (periodic)."""
+    planes = _to_dev(O.split(O.random_image(96, 80, 17)), cuda)
+    fused = dwt.Plan(w, s, optimized=opt)
+    monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
+    gen = dwt.Plan(w, s, optimized=opt)
+    assert gen.info["generic"] == 1 and fused.info["generic"] == 0
+    a, b = fused.run(planes), gen.run(planes)
+    for j in range(4):
+        assert torch_equal(a[j], b[j])
+
+
+def torch_equal(a, b):
+    import torch
+    return torch.equal(a, b)
+
+
+def test_custom_definition_wavelet_on_gpu(dwt, cuda, tmp_path):
+    """A definition-file wavelet of a new shape (generic executor) matches the
+    reference executor on the same file, bit for bit (composed lowering)."""
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    f = tmp_path / "odd.txt"
+    f.write_text("predict 0:-1/3 1:-1/3\nupdate -1:1/5 0:1/5\nscaling 1.25\n")
+    planes = O.split(O.random_image(48, 40, 3))
+    for s in FORWARD:
+        plan = dwt.Plan(str(f), s)
+        got = [t.cpu().numpy() for t in plan.run(_to_dev(planes, cuda))]
+        ref, _ = R.run(str(f), s, planes)
+        for j in range(4):
+            assert np.array_equal(got[j], ref[j]), (s, j)

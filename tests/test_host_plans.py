@@ -125,18 +125,23 @@ def test_program_tables_round_trip_through_the_abi(dwt):
 
 
 def test_definition_file_wavelet(dwt, tmp_path):
-    """A definition file equal to cdf53 resolves to the cdf53 kernel; an
-    unknown-shape file is parsed but reported unsupported (no CPU fallback)."""
+    """A definition file equal to cdf53 resolves to the cdf53 fused kernel; a
+    new shape is parsed and planned on the generic GPU executor."""
     f = tmp_path / "mine.txt"
     f.write_text("# my wavelet\nname mine\npredict 0:-1/2 1:-1/2\nupdate -1:1/4 0:1/4\nscaling 1.0\n")
     p = dwt.Plan(str(f), "separable-lifting")
     assert p.info["fingerprint"] == dwt.Plan("cdf53", "separable-lifting").info["fingerprint"]
+    assert p.info["generic"] == 0
     g = tmp_path / "odd.txt"
     g.write_text("predict 0:-1/3 1:-1/3\nupdate -1:1/5 0:1/5\n")
-    from paper_1704_08657_b200.native import DwtError
-    with pytest.raises(DwtError):
-        dwt.Plan(str(g), "separable-lifting")
+    q = dwt.Plan(str(g), "separable-lifting")
+    assert q.info["generic"] == 1 and q.info["columns_per_lane"] == 0
     bad = tmp_path / "bad.txt"
     bad.write_text("update 0:1\n")
     with pytest.raises(ValueError):
         dwt.Plan(str(bad), "separable-lifting")
+
+
+def test_symmetric_plans_use_generic_executor(dwt):
+    p = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+    assert p.info["generic"] == 1 and p.info["extension"] == 1
