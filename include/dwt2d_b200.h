@@ -209,6 +209,14 @@ DWT2D_B200_API int dwt2d_forward_mallat_host(const dwt2d_plan* plan, const float
 DWT2D_B200_API int dwt2d_inverse_mallat_host(const dwt2d_plan* inverse_plan, const float* in,
                                              int width, int height, int levels, float* image);
 
+/* --- timing (the reference's run_bench semantics, src/bench.cpp:28-44) -------
+ * Builds random_image<float>(W, H, seed) (random.hpp:31-37), uploads it once,
+ * runs one untimed warm-up and `repeats` timed transforms on the device, and
+ * returns the median seconds. levels == 1: run() on the four planar
+ * components (the reference's timed call); levels > 1: the Mallat pyramid. */
+DWT2D_B200_API int dwt2d_time_forward(const dwt2d_plan* plan, int width, int height, int levels, int repeats,
+                                      uint64_t seed, double* median_seconds);
+
 /* --- misc ------------------------------------------------------------------- */
 DWT2D_B200_API const char* dwt2d_last_error(void);
 DWT2D_B200_API const char* dwt2d_version(void);

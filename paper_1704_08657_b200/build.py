@@ -38,7 +38,7 @@ NVFLAGS = ARCH + ["-O3", "-std=c++20", "-lineinfo", "--expt-relaxed-constexpr",
 # is exported next to the C ABI
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", f"-I{INCLUDE}", "-I/usr/local/cuda/include"]
 
-HOST_SRCS = ["host/algebra.cpp", "host/wavelets.cpp", "host/schemes.cpp", "host/lowering.cpp"]
+HOST_SRCS = ["host/algebra.cpp", "host/wavelets.cpp", "host/schemes.cpp", "host/lowering.cpp", "host/io.cpp"]
 RUNTIME_SRCS = ["runtime/capi.cpp"]
 
 
@@ -124,6 +124,12 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
               "-Xlinker", "-Bsymbolic", "-Xlinker", "--exclude-libs,ALL"], BUILD / "logs" / "link.log")
+    cli_src = CSRC / "tools" / "dwt2d_cli.cpp"
+    cli_bin = PKG / "bin" / "dwt2d"
+    if force or _stale(cli_bin, [cli_src, LIB] + hdrs):
+        cli_bin.parent.mkdir(exist_ok=True)
+        _run([CXX, "-std=c++20", "-O2", f"-I{INCLUDE}", str(cli_src), "-o", str(cli_bin), f"-L{LIBDIR}",
+              "-ldwt2d_b200", "-Wl,-rpath,$ORIGIN/../lib"], BUILD / "logs" / "dwt2d_cli.log")
     test_src = ROOT / "tests" / "cpp" / "test_cpp_api.cpp"
     test_bin = BUILD / "test_cpp_api"
     if test_src.exists() and (force or _stale(test_bin, [test_src, LIB] + hdrs)):

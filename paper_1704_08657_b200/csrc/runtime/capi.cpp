@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "dwt2d_b200.h"
+#include "dwt2d_b200/image.hpp"
 #include "dwt2d_b200/lowering.hpp"
 #include "dwt2d_b200/schemes.hpp"
 #include "../kernels/level_types.hpp"
@@ -960,6 +961,71 @@ int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, in
       cuda_check(cudaMemcpyAsync(out, d_out, n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
       cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
     }
+  });
+}
+
+int dwt2d_time_forward(const dwt2d_plan* p, int W, int H, int levels, int repeats, uint64_t seed,
+                       double* median_seconds) {
+  return guard([&] {
+    require_plan(p);
+    if (!median_seconds) fail(DWT2D_EINVAL, "null argument");
+    if (repeats < 1) fail(DWT2D_EINVAL, "bench: repeats must be at least 1");
+    if (!p->forward) fail(DWT2D_EINVAL, "bench: plan is an inverse plan");
+    if (levels == 1) {
+      if (W <= 0 || H <= 0 || W % 2 || H % 2) fail(DWT2D_EINVAL, "bench: sizes must be positive and even");
+    } else {
+      check_pyramid(W, H, levels);
+    }
+    const ImagePlane<float> img = random_image<float>(W, H, seed);
+    HostPipe& hp = host_pipe();
+    const size_t n = size_t(W) * H;
+    const size_t ws_bytes = levels > 1 ? dwt2d_workspace_bytes(W, H, levels) : 0;
+    float* d = static_cast<float*>(hp.reserve(2 * n * 4 + ws_bytes + 256));
+    float* d_out = d + n;
+    float* ws = d_out + ((n + 63) & ~size_t(63));
+    const int w2 = W / 2, h2 = H / 2;
+    const size_t q = size_t(w2) * h2;
+    if (levels == 1) {  // the reference times run() on the polyphase planes
+      const PolyphaseImage<float> poly = polyphase_split(img);
+      for (int j = 0; j < 4; ++j)
+        cuda_check(cudaMemcpyAsync(d + j * q, poly.comp[j].samples.data(), q * 4, cudaMemcpyHostToDevice, hp.comp),
+                   "H2D");
+    } else {
+      cuda_check(cudaMemcpyAsync(d, img.samples.data(), n * 4, cudaMemcpyHostToDevice, hp.comp), "H2D");
+    }
+    auto once = [&] {
+      if (levels == 1) {
+        if (is_identity(*p)) return;
+        gpu::LevelArgs a{};
+        for (int j = 0; j < 4; ++j) {
+          a.in[j] = d + j * q, a.out[j] = d_out + j * q;
+          a.in_pitch[j] = a.out_pitch[j] = w2;
+        }
+        a.w2 = w2, a.h2 = h2;
+        launch(*p, a, kPlanar, hp.comp);
+      } else {
+        forward_mallat(*p, d, W, W, H, levels, d_out, W, ws, hp.comp);
+      }
+    };
+    once();
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    std::vector<double> t;
+    for (int r = 0; r < repeats; ++r) {
+      cuda_check(cudaEventRecord(e0, hp.comp), "record");
+      once();
+      cuda_check(cudaEventRecord(e1, hp.comp), "record");
+      cuda_check(cudaEventSynchronize(e1), "synchronize");
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+      t.push_back(ms * 1e-3);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::sort(t.begin(), t.end());
+    const size_t m = t.size();
+    *median_seconds = m % 2 ? t[m / 2] : 0.5 * (t[m / 2 - 1] + t[m / 2]);
   });
 }
 

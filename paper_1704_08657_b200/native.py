@@ -102,6 +102,8 @@ _SIGS = {
     "dwt2d_run_planar_host": (ctypes.c_int, [_p, _P4, _P4, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat_host": (ctypes.c_int, [_p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p]),
     "dwt2d_inverse_mallat_host": (ctypes.c_int, [_p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p]),
+    "dwt2d_time_forward": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
     "dwt2d_last_error": (ctypes.c_char_p, []),
     "dwt2d_version": (ctypes.c_char_p, []),
     "dwt2d_registry_size": (ctypes.c_int, []),

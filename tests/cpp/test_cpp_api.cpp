@@ -12,6 +12,9 @@
 #include <vector>
 
 #include "dwt2d_b200/dwt2d.hpp"
+#include "dwt2d_b200/io.hpp"
+#include <filesystem>
+#include <sstream>
 
 namespace {
 
@@ -115,6 +118,57 @@ void host_tests() {
   CHECK(fmas == 36);
 }
 
+// ------------------------------------------------------------------ io
+// (test_io.cpp cases for the PGM reader and the sub-band files)
+
+PgmError::Kind pgm_kind(const std::string& text) {
+  std::istringstream in(text);
+  try {
+    read_pgm(in);
+  } catch (const PgmError& e) {
+    return e.kind;
+  }
+  throw std::logic_error("expected a PgmError");
+}
+
+void io_tests() {
+  {
+    std::istringstream in("P2 # magic\n# a 2x3 ramp\n2 3\n255\n0 51\n102 153\n204 255\n");
+    const auto img = read_pgm(in);
+    CHECK(img.width == 2 && img.height == 3);
+    CHECK(img.at(0, 0) == 0.0);
+    CHECK(std::abs(img.at(1, 0) - 51.0 / 255.0) < 1e-15);
+    CHECK(img.at(1, 2) == 1.0);
+  }
+  {
+    std::string p5 = "P5 2 2 255\n";
+    p5 += std::string("\x00\x40\x80\xff", 4);
+    std::istringstream in(p5);
+    const auto img = read_pgm(in);
+    CHECK(img.at(1, 1) == 1.0);
+    CHECK(std::abs(img.at(1, 0) - 64.0 / 255.0) < 1e-15);
+    std::string p16 = "P5 1 1 65535\n";
+    p16 += std::string("\x80\x00", 2);
+    std::istringstream in16(p16);
+    CHECK(std::abs(read_pgm(in16).at(0, 0) - 32768.0 / 65535.0) < 1e-15);
+  }
+  CHECK(pgm_kind("P6 1 1 255\n") == PgmError::Kind::unsupported_magic);
+  CHECK(pgm_kind("P2 0 1 255\n") == PgmError::Kind::bad_header);
+  CHECK(pgm_kind("P2 2 2 70000\n0 0 0 0") == PgmError::Kind::bad_header);
+  CHECK(pgm_kind("P2 2 2 255\n0 0 0") == PgmError::Kind::truncated);
+  CHECK(pgm_kind("P5 2 2 255\n\x01") == PgmError::Kind::truncated);
+  // sub-band round trip and sidecar validation
+  const auto dir = std::filesystem::temp_directory_path() / "dwt2d_b200_subbands";
+  std::filesystem::remove_all(dir);
+  const auto p = polyphase_split(random_image<float>(12, 8, 5));
+  write_subbands(p, dir);
+  CHECK(read_subbands<float>(dir) == p);
+  check_throws<IoError>([&] { read_subbands<double>(dir); }, "precision mismatch");
+  std::filesystem::resize_file(dir / "oo.raw", 4);
+  check_throws<IoError>([&] { read_subbands<float>(dir); }, "short payload");
+  std::filesystem::remove_all(dir);
+}
+
 // ----------------------------------------------------------------- gpu
 
 void gpu_tests() {
@@ -186,6 +240,7 @@ void gpu_tests() {
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "host";
   host_tests();
+  io_tests();
   if (mode == "gpu") gpu_tests();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
