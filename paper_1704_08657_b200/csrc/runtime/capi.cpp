@@ -105,11 +105,14 @@ bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(
 
 // Rows per warp work item. A warp streams one strip of one chunk; the
 // (up + down) rows around each chunk are re-read as warm-up. Measured on
-// B200 (scripts/tune_level.cu): large levels run best with ~5 waves of work
-// items (chunk ~64 rows at 16384^2: 6.1 TB/s) — many short items keep
-// vertically adjacent chunks in flight together so their shared halo rows
-// hit L2 — while small, L2-resident levels are latency bound and want more
-// warps (chunks of 2..8 rows).
+// B200 (scripts/tune_level.cu, scripts/sweep_configs.py, bench.py): mid-size
+// levels (one wave of resident warps covers them with <= 48-row chunks) run
+// best as a single wave (4096^2 cold: 4.1 TB/s vs 3.6 with 5-row chunks);
+// large levels run best with ~5 waves (16384^2: 6.1 TB/s with 64-row
+// chunks vs 5.95 for one wave of 328-row chunks, whose concurrent accesses
+// span the whole image; 8192^2 inside the pyramid: 106 us with 16-row
+// chunks vs 113 us with one wave of 81-row chunks); tiny L2-resident levels
+// want the most warps (2-row chunks).
 int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
   if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
     const int v = std::atoi(env);
@@ -123,10 +126,10 @@ int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
   }
   const long long resident = std::max(1, cached_blocks ? cached_blocks : 2) * 4ll * sm_count();
   const long long rows_total = (long long)h2 * std::max(1, nstrips);
-  const int for_waves = int((rows_total + 5 * resident - 1) / (5 * resident));   // ~5 waves
-  const int for_fill = int(std::max(2ll, (rows_total + resident - 1) / resident));  // >= 1 wave
-  const int chunk = std::max(for_waves, std::min(8, for_fill));
-  return std::max(1, std::min(chunk, h2));
+  const long long per_warp = (rows_total + resident - 1) / resident;
+  long long chunk = per_warp <= 48 ? std::max<long long>(2, per_warp)
+                                   : (rows_total + 5 * resident - 1) / (5 * resident);
+  return int(std::max<long long>(1, std::min<long long>(chunk, h2)));
 }
 
 enum Layout { kPlanar, kFromImage, kToImage };
