@@ -541,93 +541,131 @@ HostPipe& host_pipe() {
 }
 
 int band_rows_for(int H, int halo_rows) {
-  if (const char* env = std::getenv("DWT2D_HOST_BAND_ROWS")) {
-    const int v = std::atoi(env);
-    if (v > 0 && v % 2 == 0) return std::min(v, H);
-  }
-  int r = ((H / 16) + 1) & ~1;  // ~16 bands
-  r = std::max(r, std::max(64, 2 * halo_rows));
+  int r = 0;
+  if (const char* env = std::getenv("DWT2D_HOST_BAND_ROWS")) r = std::atoi(env);
+  if (r <= 0) r = H / 16;                         // ~16 bands
+  r = std::max(r, std::max(64, 4 * halo_rows));   // level-2 bands need their own halo rows
+  r = (r + 3) & ~3;                               // even LL1 rows per band
   return std::min(r, H);
+}
+
+// One forward level on image rows [r0, r1) of a level input `in` (w_in x
+// h_in, pitch ip) whose rows above/below come from the same buffer (periodic
+// wrap): the band's rows of LL go to `ll` (pitch llp), of HL/LH/HH to the
+// level's Mallat region `det` (pitch dp).
+void band_level(const dwt2d_plan& p, const float* in, size_t ip, int w_in, int h_in, int r0, int r1, float* ll,
+                size_t llp, float* det, size_t dp, cudaStream_t st) {
+  const int top_rows = 2 * p.up, bot_rows = 2 * p.down;
+  if (r0 > 0 && r0 < top_rows) fail(DWT2D_EINVAL, "band rows smaller than the halo");
+  const float* top = r0 >= top_rows ? in + size_t(r0 - top_rows) * ip : in + size_t(h_in - top_rows) * ip;
+  const float* bot = r1 + bot_rows <= h_in ? in + size_t(r1) * ip : in;
+  const int w2 = w_in / 2, h2 = h_in / 2, y0 = r0 / 2, hb = (r1 - r0) / 2;
+  gpu::LevelArgs a{};
+  for (int j = 0; j < 4; ++j) {
+    a.in[j] = in + size_t(r0) * ip, a.in_pitch[j] = (long long)ip;
+    a.halo_top[j] = top, a.halo_bot[j] = bot;
+    a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)ip;
+  }
+  a.out[0] = ll + size_t(y0) * llp;
+  a.out_pitch[0] = (long long)llp;
+  a.out[1] = det + size_t(y0) * dp + w2;
+  a.out[2] = det + size_t(h2 + y0) * dp;
+  a.out[3] = det + size_t(h2 + y0) * dp + w2;
+  a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = (long long)dp;
+  a.halo = 1, a.up = p.up, a.down = p.down;
+  a.w2 = w2, a.h2 = hb;
+  launch(p, a, kFromImage, st);
+}
+
+// D2H of a band's detail rows of one level (Mallat region `det`/`hdet` with
+// pitch W floats, level input w_in x h_in, output component rows [y0, y0+hb))
+void band_details_down(float* hdet, const float* det, int W, int w_in, int h_in, int y0, int hb, cudaStream_t st) {
+  const int w2 = w_in / 2, h2 = h_in / 2;
+  const size_t pitch = size_t(W) * 4;
+  cuda_check(cudaMemcpy2DAsync(hdet + size_t(y0) * W + w2, pitch, det + size_t(y0) * W + w2, pitch, size_t(w2) * 4,
+                               hb, cudaMemcpyDeviceToHost, st),
+             "D2H");
+  // LH and HH rows sit side by side: one block of w_in columns
+  cuda_check(cudaMemcpy2DAsync(hdet + size_t(h2 + y0) * W, pitch, det + size_t(h2 + y0) * W, pitch, size_t(w_in) * 4,
+                               hb, cudaMemcpyDeviceToHost, st),
+             "D2H");
 }
 
 void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int W, int H, int levels,
                                    float* out) {
   HostPipe& hp = host_pipe();
-  const size_t n = size_t(W) * H, q = size_t(W / 2) * (H / 2);
-  const int top_rows = 2 * p.up, bot_rows = 2 * p.down;
-  if (top_rows > H || bot_rows > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
-  const size_t sub_ws = levels > 1 ? dwt2d_workspace_bytes(W / 2, H / 2, levels - 1) : 0;
-  const size_t bytes = (2 * n + q) * 4 + sub_ws + 256;
-  void* mem = hp.reserve(bytes);
-  float* d_img = static_cast<float*>(mem);
+  const int U = p.up, Ld = p.down;
+  const size_t n = size_t(W) * H, q = size_t(W / 2) * (H / 2), q2 = q / 4;
+  const int w2 = W / 2, h2 = H / 2, w4 = W / 4, h4 = H / 4;
+  const bool two = levels >= 2;  // level 2 is pipelined by bands as well
+  const int tail_rows = two ? 6 * U : 2 * U;  // uploaded first (periodic halos of band 0)
+  if (tail_rows + 2 * Ld > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
+  const size_t sub_ws = levels > 2 ? dwt2d_workspace_bytes(w4, h4, levels - 2) : 0;
+  const size_t bytes = (2 * n + q + q2) * 4 + sub_ws + 512;
+  float* d_img = static_cast<float*>(hp.reserve(bytes));
   float* d_out = d_img + n;
   float* d_ll1 = d_out + n;
-  float* d_sub = d_ll1 + ((q + 63) & ~size_t(63));
-  cudaEvent_t ev_alloc = hp.event(0);
+  float* d_ll2 = d_ll1 + ((q + 63) & ~size_t(63));
+  float* d_sub = d_ll2 + ((q2 + 63) & ~size_t(63));
+  size_t ev = 0;
+  cudaEvent_t ev_alloc = hp.event(ev++);
   cuda_check(cudaEventRecord(ev_alloc, hp.comp), "record");
   cuda_check(cudaStreamWaitEvent(hp.up, ev_alloc), "wait");
   cuda_check(cudaStreamWaitEvent(hp.down, ev_alloc), "wait");
 
-  const int R = band_rows_for(H, std::max(top_rows, bot_rows));
+  const int R = band_rows_for(H, std::max(U, Ld) * 2);
   const int B = (H + R - 1) / R;
-  // the image's last rows first: band 0's (periodic) top halo
-  const size_t tail0 = size_t(H - top_rows) * W;
-  cuda_check(cudaMemcpyAsync(d_img + tail0, image + tail0, size_t(top_rows) * W * 4, cudaMemcpyHostToDevice,
-                             hp.up),
+  // upload: the image's last rows first, then the bands in order
+  const size_t tail0 = size_t(H - tail_rows) * W;
+  cuda_check(cudaMemcpyAsync(d_img + tail0, image + tail0, size_t(tail_rows) * W * 4, cudaMemcpyHostToDevice, hp.up),
              "H2D");
+  std::vector<cudaEvent_t> up(B);
   for (int b = 0; b < B; ++b) {
     const int r0 = b * R, r1 = std::min(H, r0 + R);
-    const int c1 = (b == B - 1) ? std::max(r0, H - top_rows) : r1;  // tail rows already uploaded
+    const int c1 = (b == B - 1) ? std::max(r0, H - tail_rows) : r1;
     if (c1 > r0)
       cuda_check(cudaMemcpyAsync(d_img + size_t(r0) * W, image + size_t(r0) * W, size_t(c1 - r0) * W * 4,
                                  cudaMemcpyHostToDevice, hp.up),
                  "H2D");
-    cuda_check(cudaEventRecord(hp.event(1 + b), hp.up), "record");
+    up[b] = hp.event(ev++);
+    cuda_check(cudaEventRecord(up[b], hp.up), "record");
   }
-  const int w2 = W / 2, h2 = H / 2;
-  for (int b = 0; b < B; ++b) {
-    const int r0 = b * R, r1 = std::min(H, r0 + R);
-    // band b needs its own rows and the first rows of band b + 1 (its bottom halo)
-    cuda_check(cudaStreamWaitEvent(hp.comp, hp.event(1 + std::min(b + 1, B - 1))), "wait");
-    gpu::LevelArgs a{};
-    const float* top = r0 >= top_rows ? d_img + size_t(r0 - top_rows) * W : d_img + tail0;
-    const float* bot = r1 + bot_rows <= H ? d_img + size_t(r1) * W : d_img;
-    if (r0 < top_rows && r0 > 0) fail(DWT2D_EINVAL, "band rows smaller than the halo");
-    const int y0 = r0 / 2, hb = (r1 - r0) / 2;
-    for (int j = 0; j < 4; ++j) {
-      a.in[j] = d_img + size_t(r0) * W, a.in_pitch[j] = W;
-      a.halo_top[j] = top, a.halo_bot[j] = bot;
-      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = W;
-    }
-    a.out[0] = (levels == 1 ? d_out + size_t(y0) * W : d_ll1 + size_t(y0) * w2);
-    a.out_pitch[0] = levels == 1 ? W : w2;
-    a.out[1] = d_out + size_t(y0) * W + w2;
-    a.out[2] = d_out + size_t(h2 + y0) * W;
-    a.out[3] = d_out + size_t(h2 + y0) * W + w2;
-    a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = W;
-    a.halo = 1, a.up = p.up, a.down = p.down;
-    a.w2 = w2, a.h2 = hb;
-    launch(p, a, kFromImage, hp.comp);
-    cudaEvent_t done = hp.event(1 + B + b);
+  float* ll1 = two ? d_ll1 : d_out;  // a one-level pyramid writes LL straight into place
+  const size_t ll1p = two ? size_t(w2) : size_t(W);
+  float* ll2 = levels == 2 ? d_out : d_ll2;
+  const size_t ll2p = levels == 2 ? size_t(W) : size_t(w4);
+
+  auto down_after = [&](auto&& copy) {
+    cudaEvent_t done = hp.event(ev++);
     cuda_check(cudaEventRecord(done, hp.comp), "record");
     cuda_check(cudaStreamWaitEvent(hp.down, done), "wait");
-    // the band's rows of HL, LH, HH
-    const size_t pitch = size_t(W) * 4;
-    cuda_check(cudaMemcpy2DAsync(out + size_t(y0) * W + w2, pitch, d_out + size_t(y0) * W + w2, pitch,
-                                 size_t(w2) * 4, hb, cudaMemcpyDeviceToHost, hp.down),
-               "D2H");
-    cuda_check(cudaMemcpy2DAsync(out + size_t(h2 + y0) * W, pitch, d_out + size_t(h2 + y0) * W, pitch,
-                                 size_t(W) * 4, hb, cudaMemcpyDeviceToHost, hp.down),
-               "D2H");
+    copy();
+  };
+  auto level2_band = [&](int b) {
+    const int r0 = (b * R) / 2, r1 = std::min(H, b * R + R) / 2;  // LL1 rows of band b
+    band_level(p, d_ll1, size_t(w2), w2, h2, r0, r1, ll2, ll2p, d_out, size_t(W), hp.comp);
+    down_after([&] { band_details_down(out, d_out, W, w2, h2, r0 / 2, (r1 - r0) / 2, hp.down); });
+  };
+
+  if (two) {  // LL1's last 2U rows early: band 0's periodic top halo at level 2
+    cuda_check(cudaStreamWaitEvent(hp.comp, up[0]), "wait");
+    band_level(p, d_img, size_t(W), W, H, H - 4 * U, H, ll1, ll1p, d_out, size_t(W), hp.comp);
   }
-  if (levels > 1)
-    forward_mallat(p, d_ll1, size_t(w2), w2, h2, levels - 1, d_out, size_t(W), d_sub, hp.comp);
-  cudaEvent_t fin = hp.event(1 + 2 * B);
-  cuda_check(cudaEventRecord(fin, hp.comp), "record");
-  cuda_check(cudaStreamWaitEvent(hp.down, fin), "wait");
-  cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(w2) * 4, h2,
-                               cudaMemcpyDeviceToHost, hp.down),
-             "D2H");
+  for (int b = 0; b < B; ++b) {
+    const int r0 = b * R, r1 = std::min(H, r0 + R);
+    cuda_check(cudaStreamWaitEvent(hp.comp, up[std::min(b + 1, B - 1)]), "wait");  // bottom halo = band b + 1
+    band_level(p, d_img, size_t(W), W, H, r0, r1, ll1, ll1p, d_out, size_t(W), hp.comp);
+    down_after([&] { band_details_down(out, d_out, W, W, H, r0 / 2, (r1 - r0) / 2, hp.down); });
+    if (two && b >= 1) level2_band(b - 1);  // its bottom halo (LL1 of band b) is ready now
+  }
+  if (two) level2_band(B - 1);
+  if (levels > 2) forward_mallat(p, d_ll2, size_t(w4), w4, h4, levels - 2, d_out, size_t(W), d_sub, hp.comp);
+  const int wq = two ? w4 : w2, hq = two ? h4 : h2;  // the remaining top-left corner
+  down_after([&] {
+    cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(wq) * 4, hq,
+                                 cudaMemcpyDeviceToHost, hp.down),
+               "D2H");
+  });
   cuda_check(cudaStreamSynchronize(hp.down), "synchronize");
 }
 
