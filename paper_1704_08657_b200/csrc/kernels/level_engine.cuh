@@ -150,10 +150,14 @@ struct Sched {
   }
 };
 
-template <class P, int PF, int s, int u, int D, int CW>
+// UPW: rows stream bottom-up (the newest window row is the topmost one), so
+// a tap at row offset dn is (dn - min_dn) rows older than the newest instead
+// of (max_dn - dn). Same taps, same order: identical results.
+template <class P, int PF, int s, int u, int D, int CW, bool UPW>
 __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW]) {
   using SC = Sched<P, PF>;
-  constexpr int nhi = Meta<P>::nhi(s);
+  constexpr int nhi = UPW ? -Meta<P>::nlo(s) : Meta<P>::nhi(s);  // age of the dn = 0 row
+  constexpr int dsign = UPW ? -1 : 1;
   constexpr int dst = SC::slot(s + 1, u, 0);
   sfor<0, 4>([&](auto R_) {
     constexpr int r = decltype(R_)::value;
@@ -178,7 +182,7 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
         constexpr int ti = decltype(T_)::value;
         constexpr TapDesc t = P::taps[ti];
         // scalar copies: nested lambdas may only use scalar constexpr locals
-        constexpr int k = SC::slot(s, u, nhi - t.dn), j = t.j, dm = t.dm;
+        constexpr int k = SC::slot(s, u, nhi - dsign * t.dn), j = t.j, dm = t.dm;
         constexpr float w = t.w;
         constexpr bool first = ti == tb;
         sfor<0, CW>([&](auto C_) {
@@ -236,7 +240,7 @@ __device__ __forceinline__ float ld1(const float* p) {
 
 // COH: loads bypass the non-coherent path (needed when the input was written
 // earlier in the same launch, i.e. by a previous level of the tail kernel).
-template <int CW, bool IL, bool VEC, bool COH = false>
+template <int CW, bool IL, bool VEC, bool COH = false, bool UPW = false>
 struct RowReader {
   static constexpr int NP = IL ? 1 : 4;  // row pointers kept
   const float* rowp[NP];  // start of the current row (+ lane column for VEC)
@@ -251,15 +255,16 @@ struct RowReader {
     const float* const* src = a.in;
     const long long* sp = a.in_pitch;
     int r = row;
+    // next_switch: the first row (in streaming order) outside this segment
     if (a.halo && row < 0) {
       src = a.halo_top, sp = a.halo_top_pitch, r = row + a.up;
-      next_switch = 0;
+      next_switch = UPW ? int(0x80000000) : 0;
     } else if (a.halo && row >= a.h2) {
       src = a.halo_bot, sp = a.halo_bot_pitch, r = row - a.h2;
-      next_switch = 0x7fffffff;
+      next_switch = UPW ? a.h2 - 1 : 0x7fffffff;
     } else {
       r = a.halo ? row : wrap(row, a.h2);
-      next_switch = a.halo ? a.h2 : row - r + a.h2;
+      next_switch = UPW ? (a.halo ? -1 : row - r - 1) : (a.halo ? a.h2 : row - r + a.h2);
     }
     sfor<0, NP>([&](auto J_) {
       constexpr int j = decltype(J_)::value;
@@ -277,10 +282,14 @@ struct RowReader {
   }
 
   __device__ __forceinline__ void advance(const LevelArgs& a) {
-    if (++n == next_switch) {
+    n += UPW ? -1 : 1;
+    if (n == next_switch) {
       seek(a, n);
     } else {
-      sfor<0, NP>([&](auto J_) { rowp[decltype(J_)::value] += pitch[decltype(J_)::value]; });
+      sfor<0, NP>([&](auto J_) {
+        if constexpr (UPW) rowp[decltype(J_)::value] -= pitch[decltype(J_)::value];
+        else rowp[decltype(J_)::value] += pitch[decltype(J_)::value];
+      });
     }
   }
 
@@ -340,7 +349,7 @@ __device__ __forceinline__ void st_vec(float* p, float2 v, bool stream) {
 }
 
 // Writes output rows y0, y0 + 1, ... (no wrap); pointers advance per row.
-template <int CW, bool IL, bool VEC>
+template <int CW, bool IL, bool VEC, bool UPW = false>
 struct RowWriter {
   float* p[4];
   long long pitch[4];
@@ -361,10 +370,11 @@ struct RowWriter {
   }
 
   __device__ __forceinline__ void advance() {
+    constexpr long long sg = UPW ? -1 : 1;
     if constexpr (IL) {
-      p[0] += 2 * pitch[0];
+      p[0] += sg * 2 * pitch[0];
     } else {
-      sfor<0, 4>([&](auto J_) { p[decltype(J_)::value] += pitch[decltype(J_)::value]; });
+      sfor<0, 4>([&](auto J_) { p[decltype(J_)::value] += sg * pitch[decltype(J_)::value]; });
     }
   }
 
@@ -415,19 +425,21 @@ struct RowWriter {
 
 // ------------------------------------------------------------- kernel
 
-// One work item: warp `wid` streams its (strip, chunk) of the level.
-template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH>
-__device__ __forceinline__ void level_item(const LevelArgs& a, const int wid) {
+// One work item: warp `wid` streams its (strip, chunk) of the level, top-down
+// or (UPW) bottom-up.
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool UPW>
+__device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, const int chunk) {
   using M = Meta<P>;
   using SC = Sched<P, PF>;
   constexpr int S = M::S, CW = M::CW, D = SC::D, UNR = SC::UNR, NS0 = SC::slots(0);
   const int lane = threadIdx.x & 31;
   const int strip = wid % a.nstrips;
-  const int chunk = a.reverse ? a.nchunks - 1 - wid / a.nstrips : wid / a.nstrips;
   const int xc = (strip * kOutLanes - 1 + lane) * CW;  // first component column of this lane
   const int y0 = chunk * a.chunk_rows;
   const int y1 = min(a.h2, y0 + a.chunk_rows);
-  const int n0 = y0 - M::U;  // first input row streamed
+  // first input row streamed, and the output row of iteration 0
+  const int n0 = UPW ? y1 - 1 + M::L : y0 - M::U;
+  const int yfirst = UPW ? n0 + M::U : n0 - M::L;
   const int rows = (y1 - y0) + M::U + M::L;
   const int iters = (rows + UNR - 1) / UNR * UNR;
   bool out_lane = lane >= 1 && lane <= kOutLanes;
@@ -443,10 +455,10 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid) {
     });
   });
 
-  RowReader<CW, IN_IL, VEC, COH> rd;
+  RowReader<CW, IN_IL, VEC, COH, UPW> rd;
   rd.init(a, xc, n0);
-  RowWriter<CW, OUT_IL, VEC> wr;
-  wr.init(a, xc, n0 - M::L);
+  RowWriter<CW, OUT_IL, VEC, UPW> wr;
+  wr.init(a, xc, yfirst);
   out_lane = out_lane && wr.lane_in_range();
   // prologue: rows n0 .. n0+PF-1 land in the slots iteration 0.. expect
   sfor<0, PF>([&](auto U_) {
@@ -473,11 +485,11 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid) {
           });
         });
       }
-      eval_step<P, PF, 0, u, D, CW>(ring);
+      eval_step<P, PF, 0, u, D, CW, UPW>(ring);
       // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
       if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW>(ring); });
-      const int y = n0 + i - M::L;
+      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW>(ring); });
+      const int y = UPW ? yfirst - i : yfirst + i;
       if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
       wr.advance();
     });
@@ -485,12 +497,26 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid) {
   (void)NS0;
 }
 
+// Chunk order and direction. With `alternate`, odd chunks stream bottom-up:
+// two vertically adjacent chunks then reach their shared boundary rows at the
+// same time (both start there, or both end there), so the warm-up rows one of
+// them re-reads are still in L2 instead of coming from HBM again.
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH>
+__device__ __forceinline__ void level_dispatch(const LevelArgs& a, const int wid) {
+  const int c = wid / a.nstrips;
+  const int chunk = a.reverse ? a.nchunks - 1 - c : c;
+  if (a.alternate && (chunk & 1))
+    level_item<P, PF, IN_IL, OUT_IL, VEC, COH, true>(a, wid, chunk);
+  else
+    level_item<P, PF, IN_IL, OUT_IL, VEC, COH, false>(a, wid, chunk);
+}
+
 template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
 level_kernel(const LevelArgs a) {
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  level_item<P, PF, IN_IL, OUT_IL, VEC, false>(a, wid);
+  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false>(a, wid);
 }
 
 // The deep, L2-resident levels of a pyramid in ONE cooperative launch: every
@@ -509,9 +535,9 @@ tail_kernel(const __grid_constant__ TailArgs t) {
     const int items = a.nstrips * a.nchunks;
     for (int w = gw; w < items; w += nw) {  // warp-uniform trip count
       if (a.vec)
-        level_item<P, PF, IN_IL, OUT_IL, true, true>(a, w);
+        level_dispatch<P, PF, IN_IL, OUT_IL, true, true>(a, w);
       else
-        level_item<P, PF, IN_IL, OUT_IL, false, true>(a, w);
+        level_dispatch<P, PF, IN_IL, OUT_IL, false, true>(a, w);
     }
     if (l + 1 < t.nlev) cooperative_groups::this_grid().sync();
   }

@@ -135,8 +135,14 @@ int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
 enum Layout { kPlanar, kFromImage, kToImage };
 
 // Work decomposition and vector-path eligibility of one level launch.
+bool alternate_chunks() {
+  const char* env = std::getenv("DWT2D_ALTERNATE");
+  return !(env && *env == '0');
+}
+
 void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_override = 0) {
   if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+  a.alternate = alternate_chunks() ? 1 : 0;
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
