@@ -500,15 +500,21 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
 // Chunk order and direction. With `alternate`, odd chunks stream bottom-up:
 // two vertically adjacent chunks then reach their shared boundary rows at the
 // same time (both start there, or both end there), so the warm-up rows one of
-// them re-reads are still in L2 instead of coming from HBM again.
-template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH>
+// them re-reads are still in L2 instead of coming from HBM again. Only the
+// vector kernels of the per-level launches carry the bottom-up variant (ALT):
+// it is a bandwidth optimisation for large levels, and every extra body of a
+// fully unrolled plan costs minutes of nvcc time.
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool ALT>
 __device__ __forceinline__ void level_dispatch(const LevelArgs& a, const int wid) {
   const int c = wid / a.nstrips;
   const int chunk = a.reverse ? a.nchunks - 1 - c : c;
-  if (a.alternate && (chunk & 1))
-    level_item<P, PF, IN_IL, OUT_IL, VEC, COH, true>(a, wid, chunk);
-  else
-    level_item<P, PF, IN_IL, OUT_IL, VEC, COH, false>(a, wid, chunk);
+  if constexpr (ALT) {
+    if (a.alternate && (chunk & 1)) {
+      level_item<P, PF, IN_IL, OUT_IL, VEC, COH, true>(a, wid, chunk);
+      return;
+    }
+  }
+  level_item<P, PF, IN_IL, OUT_IL, VEC, COH, false>(a, wid, chunk);
 }
 
 template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
 level_kernel(const LevelArgs a) {
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false>(a, wid);
+  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC>(a, wid);
 }
 
 // The deep, L2-resident levels of a pyramid in ONE cooperative launch: every
@@ -535,9 +541,9 @@ tail_kernel(const __grid_constant__ TailArgs t) {
     const int items = a.nstrips * a.nchunks;
     for (int w = gw; w < items; w += nw) {  // warp-uniform trip count
       if (a.vec)
-        level_dispatch<P, PF, IN_IL, OUT_IL, true, true>(a, w);
+        level_dispatch<P, PF, IN_IL, OUT_IL, true, true, false>(a, w);
       else
-        level_dispatch<P, PF, IN_IL, OUT_IL, false, true>(a, w);
+        level_dispatch<P, PF, IN_IL, OUT_IL, false, true, false>(a, w);
     }
     if (l + 1 < t.nlev) cooperative_groups::this_grid().sync();
   }

@@ -184,7 +184,7 @@ def test_host_entry_points_match_device(dwt, cuda):
 
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
-                                     ("dd137", "nonseparable-polyconvolution", False),
+                                     ("dd137", "separable-convolution", True),
                                      ("cdf97", "nonseparable-convolution", True)])
 def test_fused_tail_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     """Deep levels fused into one cooperative launch give the same bits as

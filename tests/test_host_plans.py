@@ -107,11 +107,19 @@ def test_plan_errors(dwt):
 def test_every_builtin_program_has_a_kernel(dwt):
     from paper_1704_08657_b200 import native
     keys = native.registry_keys()
-    assert len(keys) == 33
+    # the DD 13/7 non-separable convolutions (>200 taps/quad, 7x7 windows)
+    # run on the generic executor: their unrolled fused bodies take cicc
+    # over 30 minutes (gen_plans.cpp)
+    heavy = {("dd137", s) for s in ("nonseparable-convolution", "nonseparable-polyconvolution")}
+    assert len(keys) == 33 - 4
     for w in WAVELETS:
         for s in O.SCHEMES:
             for opt in (False, True):
-                assert dwt.Plan(w, s, optimized=opt).info["columns_per_lane"] in (2, 4)
+                info = dwt.Plan(w, s, optimized=opt).info
+                if (w, s) in heavy:
+                    assert info["generic"] == 1 and info["columns_per_lane"] == 0
+                else:
+                    assert info["generic"] == 0 and info["columns_per_lane"] in (2, 4)
 
 
 def test_program_tables_round_trip_through_the_abi(dwt):
