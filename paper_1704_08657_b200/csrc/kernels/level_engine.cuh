@@ -29,7 +29,6 @@
 // intermediates (executor.hpp:159-167) exactly.
 #pragma once
 
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -525,27 +524,131 @@ level_kernel(const LevelArgs a) {
   level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC>(a, wid);
 }
 
-// The deep, L2-resident levels of a pyramid in ONE cooperative launch: every
-// warp grid-strides over each level's work items, and a grid-wide barrier
-// separates consecutive levels (their LL feeds the next). Replaces a chain of
-// latency-bound launches whose per-level cost is a few microseconds of
-// launch and pipeline fill each. Loads use the coherent L2 path because the
-// inputs of levels 2.. are written inside this launch.
+// ------------------------------------------------ wavefront pyramid kernel
+//
+// A whole forward Mallat pyramid in ONE persistent launch, scheduled as a
+// dataflow wavefront instead of level after level. Work items are the same
+// (level, strip, chunk) warp items as above. Level l + 1's chunk c becomes
+// claimable as soon as the level-l chunks holding the LL_l rows it reads
+// (its rows plus the up/down reach, periodic wrap) are complete, so:
+//   * LL_l rows are consumed a few microseconds after they were written, from
+//     L2 — the next level's input never comes back from HBM;
+//   * the latency-bound deep levels run in the shadow of the bandwidth-bound
+//     level 1 instead of as a chain of small launches after it.
+// Scheduling (no warp ever waits on an unclaimed item, so no deadlock): each
+// level hands out its items in the order chunk n-1, 0, 1, ..., n-2 (the last
+// chunk first: the first chunk of the next level wraps onto it). A warp
+// prefers the deepest level whose next item is ready, claims it by
+// compare-and-swap on the level's head counter, and otherwise takes the next
+// level-0 item (never blocked). Completion is counted per (level, chunk) in
+// strips; the producer releases with a fence before the count, consumers
+// acquire and then read with L2-coherent loads (COH).
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int wave_chunk(const LevelArgs& a, unsigned item) {
+  const int pos = int(item / unsigned(a.nstrips));
+  return pos == 0 ? a.nchunks - 1 : pos - 1;
+}
+
+// Level-(l-1) chunks whose LL rows level l's chunk c reads: one or two
+// contiguous ranges [lo0, hi0], [lo1, hi1] (periodic wrap); lo1 > hi1 if none.
+template <int U, int L>
+__device__ __forceinline__ void wave_deps(const LevelArgs& a, const LevelArgs& prev, int c, int& lo0, int& hi0,
+                                          int& lo1, int& hi1) {
+  const int y0 = c * a.chunk_rows, y1 = min(a.h2, y0 + a.chunk_rows);
+  const int n = prev.h2;  // LL rows of the level below (= 2 * a.h2)
+  const int span = 2 * (y1 - 1 + L) + 1 - 2 * (y0 - U);  // last - first row
+  lo1 = 1, hi1 = 0;
+  if (span + 1 >= n) {
+    lo0 = 0, hi0 = prev.nchunks - 1;
+    return;
+  }
+  const int r0 = wrap(2 * (y0 - U), n), r1 = r0 + span;
+  if (r1 < n) {
+    lo0 = r0 / prev.chunk_rows, hi0 = r1 / prev.chunk_rows;
+  } else {
+    lo0 = r0 / prev.chunk_rows, hi0 = prev.nchunks - 1;
+    lo1 = 0, hi1 = (r1 - n) / prev.chunk_rows;
+  }
+}
+
 template <class P, int PF, bool IN_IL, bool OUT_IL>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
-tail_kernel(const __grid_constant__ TailArgs t) {
-  const int gw = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-  const int nw = gridDim.x * kWarpsPerCta;
-  for (int l = 0; l < t.nlev; ++l) {
-    const LevelArgs& a = t.lv[l];
-    const int items = a.nstrips * a.nchunks;
-    for (int w = gw; w < items; w += nw) {  // warp-uniform trip count
-      if (a.vec)
-        level_dispatch<P, PF, IN_IL, OUT_IL, true, true, false>(a, w);
-      else
-        level_dispatch<P, PF, IN_IL, OUT_IL, false, true, false>(a, w);
+wave_kernel(const __grid_constant__ WaveArgs t) {
+  using M = Meta<P>;
+  const int lane = threadIdx.x & 31;
+  unsigned* head = t.state;
+  const unsigned full = 0xffffffffu;
+  for (;;) {
+    // one round trip: lane l reads level l's head
+    unsigned h = 0, total = 0;
+    if (lane < t.nlev) {
+      h = ld_relaxed(head + lane);
+      total = unsigned(t.lv[lane].nstrips) * unsigned(t.lv[lane].nchunks);
     }
-    if (l + 1 < t.nlev) cooperative_groups::this_grid().sync();
+    const unsigned open = __ballot_sync(full, lane < t.nlev && h < total);
+    if (!open) break;
+    // quick readiness filter: lane l >= 1 checks the furthest level-(l-1)
+    // chunk its next item needs (chunks complete roughly in order)
+    bool quick = false;
+    if (lane >= 1 && lane < t.nlev && ((open >> lane) & 1u)) {
+      int lo0, hi0, lo1, hi1;
+      wave_deps<M::U, M::L>(t.lv[lane], t.lv[lane - 1], wave_chunk(t.lv[lane], h), lo0, hi0, lo1, hi1);
+      const int probe = lo1 <= hi1 ? hi1 : hi0;
+      quick = ld_relaxed(t.state + t.done_off[lane - 1] + probe) >= unsigned(t.lv[lane - 1].nstrips);
+    }
+    unsigned cand = __ballot_sync(full, quick);
+    int lvl = -1;
+    unsigned item = 0;
+    while (cand) {  // deepest ready level first
+      const int l = 31 - __clz(cand);
+      cand &= ~(1u << l);
+      const unsigned hh = __shfl_sync(full, h, l);
+      int lo0, hi0, lo1, hi1;
+      wave_deps<M::U, M::L>(t.lv[l], t.lv[l - 1], wave_chunk(t.lv[l], hh), lo0, hi0, lo1, hi1);
+      const unsigned need = unsigned(t.lv[l - 1].nstrips);
+      const unsigned* done = t.state + t.done_off[l - 1];
+      bool ok = true;
+      for (int k = lo0 + lane; k <= hi0; k += 32) ok = ok && ld_acquire(done + k) >= need;
+      for (int k = lo1 + lane; k <= hi1; k += 32) ok = ok && ld_acquire(done + k) >= need;
+      if (!__all_sync(full, ok)) continue;
+      unsigned old = 0;
+      if (lane == 0) old = atomicCAS(head + l, hh, hh + 1);
+      old = __shfl_sync(full, old, 0);
+      if (old == hh) {
+        lvl = l, item = hh;
+        break;
+      }
+    }
+    if (lvl < 0 && (open & 1u)) {
+      unsigned i = 0;
+      if (lane == 0) i = atomicAdd(head, 1u);
+      i = __shfl_sync(full, i, 0);
+      if (i < unsigned(t.lv[0].nstrips) * unsigned(t.lv[0].nchunks)) lvl = 0, item = i;
+    }
+    if (lvl < 0) {
+      __nanosleep(256);
+      continue;
+    }
+    const LevelArgs& a = t.lv[lvl];
+    const int strip = int(item % unsigned(a.nstrips));
+    const int chunk = wave_chunk(a, item);
+    if (a.alternate && (chunk & 1))
+      level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
+    else
+      level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(t.state + t.done_off[lvl] + chunk, 1u);
   }
 }
 

@@ -52,13 +52,19 @@ struct LevelArgs {
 
 using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
 
-constexpr int kMaxTailLevels = 12;
-struct TailArgs {
-  LevelArgs lv[kMaxTailLevels];
+// Wavefront pyramid (level_engine.cuh: wave_kernel): every level of a
+// forward pyramid in one persistent launch. `state` (device, zeroed before
+// the launch) holds nlev head counters, then per level one completion
+// counter per chunk starting at done_off[l].
+constexpr int kMaxWaveLevels = 16;
+struct WaveArgs {
+  LevelArgs lv[kMaxWaveLevels];
   int nlev;
+  unsigned* state;
+  int done_off[kMaxWaveLevels];
 };
-// cooperative launch of the fused deep-level kernel; grid = `blocks` CTAs
-using TailLaunch = cudaError_t (*)(const TailArgs&, int blocks, cudaStream_t);
+// persistent launch of the wavefront kernel; grid = `blocks` CTAs
+using WaveLaunch = cudaError_t (*)(const WaveArgs&, int blocks, cudaStream_t);
 // resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
 using LevelOccupancy = int (*)();
 
@@ -72,8 +78,8 @@ struct PlanEntry {
   LevelLaunch from_image;      // interleaved -> 4 planes (forward levels)
   LevelLaunch to_image;        // 4 planes -> interleaved (inverse levels)
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
-  TailLaunch tail;             // fused deep levels (same direction as from_image/to_image)
-  LevelOccupancy tail_occupancy;
+  WaveLaunch wave;             // whole forward pyramid in one launch (forward plans)
+  LevelOccupancy wave_occupancy;
 };
 
 // One sub-step of the generic executor (kernels/generic_step.cu). `taps`

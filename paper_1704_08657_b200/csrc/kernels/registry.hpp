@@ -39,17 +39,16 @@ int level_occupancy() {
   return blocks;
 }
 
-template <class P, bool IN_IL, bool OUT_IL>
-cudaError_t launch_tail(const TailArgs& t, int blocks, cudaStream_t st) {
-  void* args[] = {const_cast<TailArgs*>(&t)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&tail_kernel<P, kPrefetchRows, IN_IL, OUT_IL>),
-                                     dim3(blocks), dim3(kWarpsPerCta * 32), args, 0, st);
+template <class P>
+cudaError_t launch_wave(const WaveArgs& t, int blocks, cudaStream_t st) {
+  wave_kernel<P, kPrefetchRows, true, false><<<blocks, kWarpsPerCta * 32, 0, st>>>(t);
+  return cudaGetLastError();
 }
 
-template <class P, bool IN_IL, bool OUT_IL>
-int tail_occupancy() {
+template <class P>
+int wave_occupancy() {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tail_kernel<P, kPrefetchRows, IN_IL, OUT_IL>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, wave_kernel<P, kPrefetchRows, true, false>,
                                                     kWarpsPerCta * 32, 0) != cudaSuccess) {
     cudaGetLastError();
     return 0;
@@ -70,13 +69,11 @@ PlanEntry make_entry() {
   if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;
     e.occupancy = &level_occupancy<P, true, false>;
-    e.tail = &launch_tail<P, true, false>;
-    e.tail_occupancy = &tail_occupancy<P, true, false>;
+    e.wave = &launch_wave<P>;
+    e.wave_occupancy = &wave_occupancy<P>;
   } else {
     e.to_image = &launch_level<P, false, true>;
     e.occupancy = &level_occupancy<P, false, true>;
-    e.tail = &launch_tail<P, false, true>;
-    e.tail_occupancy = &tail_occupancy<P, false, true>;
   }
   return e;
 }

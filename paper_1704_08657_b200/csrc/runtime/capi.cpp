@@ -252,43 +252,6 @@ void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t s
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-// Levels whose input is at most this many bytes run fused in one cooperative
-// tail launch (they are L2-resident and latency bound). DWT2D_TAIL_BYTES
-// overrides; 0 disables the tail.
-size_t tail_bytes() {
-  if (const char* env = std::getenv("DWT2D_TAIL_BYTES")) return size_t(std::atoll(env));
-  return 0;  // measured: no faster than per-level launches on B200
-}
-
-// Launches the levels in `lv` (already filled, consecutive, same direction)
-// as one cooperative kernel.
-void launch_tail(const dwt2d_plan& p, std::vector<gpu::LevelArgs>& lv, Layout layout, cudaStream_t st) {
-  const gpu::PlanEntry& e = *p.entry;
-  static thread_local const gpu::PlanEntry* cached = nullptr;
-  static thread_local int per_sm = 0;
-  if (cached != &e) {
-    cached = &e;
-    per_sm = e.tail_occupancy ? e.tail_occupancy() : 0;
-  }
-  if (per_sm <= 0) fail(DWT2D_ECUDA, "tail kernel cannot be resident");
-  const int blocks = per_sm * sm_count();
-  const long long warps = (long long)blocks * gpu::kWarpsPerCta;
-  gpu::TailArgs t{};
-  t.nlev = int(lv.size());
-  for (size_t i = 0; i < lv.size(); ++i) {
-    gpu::LevelArgs& a = lv[i];
-    const int cw = e.cw;
-    const int nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
-    // one pass of the grid's warps over the level's work items
-    const long long rows = (long long)a.h2 * nstrips;
-    const int chunk = int(std::max<long long>(2, (rows + warps - 1) / warps));
-    prepare(p, a, layout, chunk);
-    t.lv[i] = a;
-  }
-  cuda_check(e.tail(t, blocks, st), "tail kernel launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
 bool is_identity(const dwt2d_plan& p) { return !p.entry && !p.generic; }
 
 void require_plan(const dwt2d_plan* p) {
@@ -377,11 +340,18 @@ void check_pyramid(int W, int H, int levels) {
     fail(DWT2D_EINVAL, "pyramid: width and height must be divisible by 2^levels");
 }
 
-// intermediate LL band of level k (k >= 1) in the workspace: odd k at A, even at B
-float* ll_slot(float* ws, int W, int H, int k) {
-  const size_t a = size_t(W / 2) * size_t(H / 2);
-  return (k & 1) ? ws : ws + ((a + 63) & ~size_t(63));
+// Workspace layout (dwt2d_workspace_bytes): the intermediate LL band of every
+// level k = 1 .. levels-1 in its own slot (the wavefront kernel has all levels
+// in flight at once), then the wavefront's scheduling counters.
+size_t ws_align(size_t floats) { return (floats + 63) & ~size_t(63); }
+size_t ll_offset(int W, int H, int k) {
+  size_t off = 0;
+  for (int i = 1; i < k; ++i) off += ws_align(size_t(W >> i) * size_t(H >> i));
+  return off;
 }
+float* ll_slot(float* ws, int W, int H, int k) { return ws + ll_offset(W, H, k); }
+// counters: one head per level + one per chunk (chunks <= rows of the level)
+size_t wave_state_words(int H, int levels) { return ws_align(size_t(levels) + size_t(H)); }
 
 struct Workspace {
   float* ptr = nullptr;
@@ -413,49 +383,96 @@ void record(void* ev, cudaStream_t st) {
   cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, flags), "event record");
 }
 
+// The wavefront kernel runs the whole pyramid when every level can take the
+// vector path (sides divisible by 4 * 2^levels for CW = 4, aligned buffers).
+// DWT2D_WAVEFRONT=0 selects one launch per level.
+bool wavefront_enabled() {
+  const char* env = std::getenv("DWT2D_WAVEFRONT");
+  return !(env && *env == '0');
+}
+
+// Rows per work item of level l inside the wavefront (DWT2D_WAVE_CHUNK_ROWS
+// overrides the deep levels): level 1 keeps the per-level policy; deeper
+// levels use short chunks so the end-of-pyramid drain (one item per level)
+// stays short.
+int wave_chunk_rows(const dwt2d_plan& p, int l, int h2, int nstrips) {
+  if (l == 1) return chunk_rows_for(p, h2, nstrips);
+  int v = 16;
+  if (const char* env = std::getenv("DWT2D_WAVE_CHUNK_ROWS")) v = std::max(1, std::atoi(env));
+  return std::min(v, h2);
+}
+
+void fill_forward_level(gpu::LevelArgs& a, const float* cur, size_t cur_pitch, float* ll, size_t ll_pitch,
+                        float* out, size_t out_pitch, int w2, int h2) {
+  a = gpu::LevelArgs{};
+  a.in[0] = a.in[1] = a.in[2] = a.in[3] = cur;
+  for (int j = 0; j < 4; ++j) a.in_pitch[j] = (long long)cur_pitch;
+  a.out[0] = ll;
+  a.out_pitch[0] = (long long)ll_pitch;
+  a.out[1] = out + w2;
+  a.out[2] = out + size_t(h2) * out_pitch;
+  a.out[3] = out + size_t(h2) * out_pitch + w2;
+  a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = (long long)out_pitch;
+  a.w2 = w2, a.h2 = h2;
+}
+
 void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W, int H, int levels,
                     float* out, size_t out_pitch, float* ws, cudaStream_t st,
                     void* const* events = nullptr) {
   if (events) record(events[0], st);
+  std::vector<gpu::LevelArgs> lv(levels);
   const float* cur = image;
   size_t cur_pitch = pitch;
-  std::vector<gpu::LevelArgs> tail;
-  int tail_first = 0;
-  const size_t tail_limit = tail_bytes();
   for (int l = 1; l <= levels; ++l) {
     const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
-    gpu::LevelArgs a{};
-    a.in[0] = a.in[1] = a.in[2] = a.in[3] = cur;
-    for (int j = 0; j < 4; ++j) a.in_pitch[j] = (long long)cur_pitch;
     float* ll = l == levels ? out : ll_slot(ws, W, H, l);
     const size_t ll_pitch = l == levels ? out_pitch : size_t(w2);
-    a.out[0] = ll;
-    a.out_pitch[0] = (long long)ll_pitch;
-    a.out[1] = out + w2;
-    a.out[2] = out + size_t(h2) * out_pitch;
-    a.out[3] = out + size_t(h2) * out_pitch + w2;
-    a.out_pitch[1] = a.out_pitch[2] = a.out_pitch[3] = (long long)out_pitch;
-    a.w2 = w2, a.h2 = h2;
+    fill_forward_level(lv[l - 1], cur, cur_pitch, ll, ll_pitch, out, out_pitch, w2, h2);
+    cur = ll;
+    cur_pitch = ll_pitch;
+  }
+  bool wave = p.entry && p.entry->wave && levels >= 2 && levels <= gpu::kMaxWaveLevels && wavefront_enabled();
+  if (wave) {
+    for (int l = 1; l <= levels && wave; ++l) {
+      gpu::LevelArgs& a = lv[l - 1];
+      prepare(p, a, kFromImage);
+      const int nstrips = a.nstrips;
+      prepare(p, a, kFromImage, wave_chunk_rows(p, l, a.h2, nstrips));
+      wave = wave && a.vec;
+    }
+  }
+  if (wave) {
+    static thread_local const gpu::PlanEntry* cached = nullptr;
+    static thread_local int per_sm = 0;
+    if (cached != p.entry) {
+      cached = p.entry;
+      per_sm = p.entry->wave_occupancy ? p.entry->wave_occupancy() : 0;
+    }
+    if (per_sm <= 0) fail(DWT2D_ECUDA, "wavefront kernel cannot be resident");
+    gpu::WaveArgs t{};
+    t.nlev = levels;
+    t.state = reinterpret_cast<unsigned*>(ws + ll_offset(W, H, levels));
+    int off = levels;
+    for (int l = 0; l < levels; ++l) {
+      t.lv[l] = lv[l];
+      t.done_off[l] = off;
+      off += lv[l].nchunks;
+    }
+    cuda_check(cudaMemsetAsync(t.state, 0, size_t(off) * sizeof(unsigned), st), "wavefront counters");
+    cuda_check(p.entry->wave(t, per_sm * sm_count(), st), "wavefront kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (events)
+      for (int l = 1; l <= levels; ++l) record(events[l], st);
+    return;
+  }
+  for (int l = 1; l <= levels; ++l) {
+    gpu::LevelArgs a = lv[l - 1];
     // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
     // level l wrote last, which are still in L2 (LL uses normal stores, the
     // detail bands evict-first).
     a.reverse = (l % 2 == 0) ? 1 : 0;
-    const bool small = p.entry && size_t(w) * size_t(h) * 4 <= tail_limit && levels - l + 1 >= 2 &&
-                       levels - l + 1 <= gpu::kMaxTailLevels;
-    if (!tail.empty() || small) {
-      if (tail.empty()) tail_first = l;
-      tail.push_back(a);
-    } else {
-      launch(p, a, kFromImage, st);
-      if (events) record(events[l], st);
-    }
-    cur = ll;
-    cur_pitch = ll_pitch;
-  }
-  if (!tail.empty()) {
-    launch_tail(p, tail, kFromImage, st);
-    if (events)
-      for (int l = tail_first; l <= levels; ++l) record(events[l], st);
+    launch(p, a, kFromImage, st);
+    if (events) record(events[l], st);
   }
 }
 
@@ -464,8 +481,6 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
   const float* ll = in;
   size_t ll_pitch = in_pitch;
   if (is_identity(p)) fail(DWT2D_EUNSUPPORTED, "identity inverse pyramid");
-  std::vector<gpu::LevelArgs> tail;
-  const size_t tail_limit = tail_bytes();
   for (int l = levels; l >= 1; --l) {
     const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
     gpu::LevelArgs a{};
@@ -481,21 +496,7 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
     for (int j = 0; j < 4; ++j) a.out_pitch[j] = (long long)dst_pitch;
     a.w2 = w2, a.h2 = h2;
     a.reverse = ((levels - l) % 2 == 1) ? 1 : 0;
-    // the deepest levels come first here: batch them while they stay small
-    const bool small = p.entry && size_t(w) * size_t(h) * 4 <= tail_limit &&
-                       int(tail.size()) < gpu::kMaxTailLevels;
-    if (small && l > 1) {
-      tail.push_back(a);
-    } else {
-      if (!tail.empty()) {
-        if (tail.size() == 1)
-          launch(p, tail[0], kToImage, st);
-        else
-          launch_tail(p, tail, kToImage, st);
-        tail.clear();
-      }
-      launch(p, a, kToImage, st);
-    }
+    launch(p, a, kToImage, st);
     ll = dst;
     ll_pitch = dst_pitch;
   }
@@ -884,9 +885,7 @@ int dwt2d_inverse_level_strip(const dwt2d_plan* p, const float* const in[4], con
 
 size_t dwt2d_workspace_bytes(int width, int height, int levels) {
   if (levels < 2 || width <= 0 || height <= 0) return 0;
-  const size_t a = size_t(width / 2) * size_t(height / 2);
-  const size_t b = levels >= 3 ? size_t(width / 4) * size_t(height / 4) : 0;
-  return (((a + 63) & ~size_t(63)) + b) * sizeof(float);
+  return (ll_offset(width, height, levels) + wave_state_words(height, levels)) * sizeof(float);
 }
 
 int dwt2d_forward_mallat(const dwt2d_plan* p, const float* image, size_t pitch, int W, int H, int levels,

@@ -185,24 +185,30 @@ def test_host_entry_points_match_device(dwt, cuda):
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
                                      ("dd137", "separable-convolution", True),
-                                     ("cdf97", "nonseparable-convolution", True)])
-def test_fused_tail_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
-    """Deep levels fused into one cooperative launch give the same bits as
-    one launch per level, forward and inverse, incl. scalar-path levels."""
+                                     ("cdf97", "nonseparable-convolution", True),
+                                     ("cdf97", "nonseparable-polyconvolution", False)])
+def test_wavefront_pyramid_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+    """The whole pyramid in one wavefront launch (levels in flight together,
+    dataflow-scheduled) gives the same bits as one launch per level, for
+    several work-item sizes incl. 1-row and ragged chunks."""
     import torch
     plan = dwt.Plan(w, s, optimized=opt)
-    inv = dwt.Plan(w, "inverse-lifting")
-    for W, H, L in [(512, 384, 7), (96, 64, 5)]:
+    for W, H, L, c1, cd in [(512, 384, 5, "0", "16"), (512, 384, 5, "7", "1"), (96, 64, 3, "3", "5"),
+                            (1024, 256, 6, "0", "3"), (256, 1024, 4, "1000", "1000")]:
         img = torch.from_numpy(O.random_image(W, H, 8)).to(cuda)
-        monkeypatch.setenv("DWT2D_TAIL_BYTES", "0")
+        monkeypatch.setenv("DWT2D_WAVEFRONT", "0")
+        monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
         a = plan.forward_mallat(img, L)
-        ia = inv.inverse_mallat(a, L)
-        monkeypatch.setenv("DWT2D_TAIL_BYTES", str(1 << 30))
-        b = plan.forward_mallat(img, L)
-        ib = inv.inverse_mallat(a, L)
+        monkeypatch.setenv("DWT2D_WAVEFRONT", "1")
+        if c1 != "0":
+            monkeypatch.setenv("DWT2D_CHUNK_ROWS", c1)
+        monkeypatch.setenv("DWT2D_WAVE_CHUNK_ROWS", cd)
+        before = dwt.launch_count()
+        for _ in range(3):  # counters are reset by every call
+            b = plan.forward_mallat(img, L)
         torch.cuda.synchronize()
-        assert torch.equal(a, b), (W, H, L)
-        assert torch.equal(ia, ib), (W, H, L)
+        assert dwt.launch_count() - before == 3, (W, H, L)
+        assert torch.equal(a, b), (W, H, L, c1, cd)
 
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-convolution", False),
@@ -278,14 +284,12 @@ def test_launch_count_and_native_library_loaded(dwt, cuda, monkeypatch):
     from paper_1704_08657_b200 import native
     plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
     img = torch.from_numpy(O.random_image(256, 256, 2)).to(cuda)
-    monkeypatch.setenv("DWT2D_TAIL_BYTES", "0")  # one launch per level
     before = dwt.launch_count()
-    plan.forward_mallat(img, 8)
+    plan.forward_mallat(img, 8)  # level 8 is 1 component wide: no vector path, one launch per level
     torch.cuda.synchronize()
     assert dwt.launch_count() - before == 8
-    monkeypatch.setenv("DWT2D_TAIL_BYTES", str(64 << 20))  # all 8 levels fused
     before = dwt.launch_count()
-    plan.forward_mallat(img, 8)
+    plan.forward_mallat(img, 6)  # wavefront: all levels in one launch
     torch.cuda.synchronize()
     assert dwt.launch_count() - before == 1
     maps = open("/proc/self/maps").read()
