@@ -528,39 +528,34 @@ level_kernel(const LevelArgs a) {
 //
 // A whole forward Mallat pyramid in ONE persistent launch, scheduled as a
 // dataflow wavefront instead of level after level. Work items are the same
-// (level, strip, chunk) warp items as above. Level l + 1's chunk c becomes
-// claimable as soon as the level-l chunks holding the LL_l rows it reads
-// (its rows plus the up/down reach, periodic wrap) are complete, so:
+// (level, strip, chunk) warp items as above, four adjacent strips per CTA;
+// each CTA takes the next entry of a host-built ticket list (capi.cpp:
+// wave_schedule) with one atomicAdd when it starts. (One CTA per ticket, not
+// a persistent loop: long-lived warps that take item after item streamed
+// 15-20 % slower on B200 in every variant tried, scripts/tune_wave.cu.)
+// A level-l item may only start once the level-(l-1) chunks holding the LL
+// rows it reads (its rows plus the up/down reach, periodic wrap) are
+// complete; the ticket list puts every item after all items it depends on,
+// and tickets are taken in CTA start order, so an item that waits only waits
+// for items already running: no deadlock. The list also lags each deep item
+// about one wave of level-1 items behind its inputs, so waits are rare until
+// the final drain. Effects:
 //   * LL_l rows are consumed a few microseconds after they were written, from
 //     L2 — the next level's input never comes back from HBM;
 //   * the latency-bound deep levels run in the shadow of the bandwidth-bound
 //     level 1 instead of as a chain of small launches after it.
-// Scheduling (no warp ever waits on an unclaimed item, so no deadlock): each
-// level hands out its items in the order chunk n-1, 0, 1, ..., n-2 (the last
-// chunk first: the first chunk of the next level wraps onto it). A warp
-// prefers the deepest level whose next item is ready, claims it by
-// compare-and-swap on the level's head counter, and otherwise takes the next
-// level-0 item (never blocked). Completion is counted per (level, chunk) in
-// strips; the producer releases with a fence before the count, consumers
-// acquire and then read with L2-coherent loads (COH).
+// Completion is counted per (level, chunk) in strips: the producer's lanes
+// fence and the count is released after a warp barrier; consumers acquire,
+// then read with L2-coherent loads (COH).
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ int wave_chunk(const LevelArgs& a, unsigned item) {
-  const int pos = int(item / unsigned(a.nstrips));
-  return pos == 0 ? a.nchunks - 1 : pos - 1;
-}
 
 // Level-(l-1) chunks whose LL rows level l's chunk c reads: one or two
 // contiguous ranges [lo0, hi0], [lo1, hi1] (periodic wrap); lo1 > hi1 if none.
+// Mirrored on the host by capi.cpp: wave_deps (the schedule builder).
 template <int U, int L>
 __device__ __forceinline__ void wave_deps(const LevelArgs& a, const LevelArgs& prev, int c, int& lo0, int& hi0,
                                           int& lo1, int& hi1) {
@@ -585,71 +580,40 @@ template <class P, int PF, bool IN_IL, bool OUT_IL>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
 wave_kernel(const __grid_constant__ WaveArgs t) {
   using M = Meta<P>;
-  const int lane = threadIdx.x & 31;
-  unsigned* head = t.state;
+  __shared__ unsigned s_ticket;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  for (;;) {
-    // one round trip: lane l reads level l's head
-    unsigned h = 0, total = 0;
-    if (lane < t.nlev) {
-      h = ld_relaxed(head + lane);
-      total = unsigned(t.lv[lane].nstrips) * unsigned(t.lv[lane].nchunks);
-    }
-    const unsigned open = __ballot_sync(full, lane < t.nlev && h < total);
-    if (!open) break;
-    // quick readiness filter: lane l >= 1 checks the furthest level-(l-1)
-    // chunk its next item needs (chunks complete roughly in order)
-    bool quick = false;
-    if (lane >= 1 && lane < t.nlev && ((open >> lane) & 1u)) {
-      int lo0, hi0, lo1, hi1;
-      wave_deps<M::U, M::L>(t.lv[lane], t.lv[lane - 1], wave_chunk(t.lv[lane], h), lo0, hi0, lo1, hi1);
-      const int probe = lo1 <= hi1 ? hi1 : hi0;
-      quick = ld_relaxed(t.state + t.done_off[lane - 1] + probe) >= unsigned(t.lv[lane - 1].nstrips);
-    }
-    unsigned cand = __ballot_sync(full, quick);
-    int lvl = -1;
-    unsigned item = 0;
-    while (cand) {  // deepest ready level first
-      const int l = 31 - __clz(cand);
-      cand &= ~(1u << l);
-      const unsigned hh = __shfl_sync(full, h, l);
-      int lo0, hi0, lo1, hi1;
-      wave_deps<M::U, M::L>(t.lv[l], t.lv[l - 1], wave_chunk(t.lv[l], hh), lo0, hi0, lo1, hi1);
-      const unsigned need = unsigned(t.lv[l - 1].nstrips);
-      const unsigned* done = t.state + t.done_off[l - 1];
+  // dynamic block index: CTAs take tickets in the order they start, so every
+  // ticket a CTA waits for belongs to a CTA that is already running
+  if (threadIdx.x == 0) s_ticket = atomicAdd(t.state, 1u);
+  __syncthreads();
+  const unsigned ticket = s_ticket;
+  if (ticket >= unsigned(t.ntickets)) return;
+  const unsigned long long e = __ldg(t.tickets + ticket);
+  const int lvl = int(e >> 56), chunk = int(e & 0xffffffffu);
+  const int strip = int((e >> 32) & 0xffffffu) * kWarpsPerCta + warp;
+  const LevelArgs& a = t.lv[lvl];
+  if (strip >= a.nstrips) return;  // warp-uniform
+  if (lvl > 0) {
+    int lo0, hi0, lo1, hi1;
+    wave_deps<M::U, M::L>(a, t.lv[lvl - 1], chunk, lo0, hi0, lo1, hi1);
+    const unsigned need = unsigned(t.lv[lvl - 1].nstrips);
+    const unsigned* done = t.state + t.done_off[lvl - 1];
+    for (;;) {
       bool ok = true;
       for (int k = lo0 + lane; k <= hi0; k += 32) ok = ok && ld_acquire(done + k) >= need;
       for (int k = lo1 + lane; k <= hi1; k += 32) ok = ok && ld_acquire(done + k) >= need;
-      if (!__all_sync(full, ok)) continue;
-      unsigned old = 0;
-      if (lane == 0) old = atomicCAS(head + l, hh, hh + 1);
-      old = __shfl_sync(full, old, 0);
-      if (old == hh) {
-        lvl = l, item = hh;
-        break;
-      }
+      if (__all_sync(full, ok)) break;
+      __nanosleep(200);
     }
-    if (lvl < 0 && (open & 1u)) {
-      unsigned i = 0;
-      if (lane == 0) i = atomicAdd(head, 1u);
-      i = __shfl_sync(full, i, 0);
-      if (i < unsigned(t.lv[0].nstrips) * unsigned(t.lv[0].nchunks)) lvl = 0, item = i;
-    }
-    if (lvl < 0) {
-      __nanosleep(256);
-      continue;
-    }
-    const LevelArgs& a = t.lv[lvl];
-    const int strip = int(item % unsigned(a.nstrips));
-    const int chunk = wave_chunk(a, item);
-    if (a.alternate && (chunk & 1))
-      level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
-    else
-      level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) atomicAdd(t.state + t.done_off[lvl] + chunk, 1u);
   }
+  if (a.alternate && (chunk & 1))
+    level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
+  else
+    level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicAdd(t.state + t.done_off[lvl] + chunk, 1u);
 }
 
 }  // namespace gpu

@@ -54,16 +54,20 @@ using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
 
 // Wavefront pyramid (level_engine.cuh: wave_kernel): every level of a
 // forward pyramid in one persistent launch. `state` (device, zeroed before
-// the launch) holds nlev head counters, then per level one completion
-// counter per chunk starting at done_off[l].
+// the launch) holds the ticket counter, then per level one completion counter
+// per chunk starting at done_off[l]. `tickets` (device) lists the CTA work
+// items in a dependency-respecting order: level << 56 | group << 32 | chunk,
+// where the CTA's warps take strips group * kWarpsPerCta + warp.
 constexpr int kMaxWaveLevels = 16;
 struct WaveArgs {
   LevelArgs lv[kMaxWaveLevels];
   int nlev;
+  int ntickets;
   unsigned* state;
+  const unsigned long long* tickets;
   int done_off[kMaxWaveLevels];
 };
-// persistent launch of the wavefront kernel; grid = `blocks` CTAs
+// launch of the wavefront kernel; grid = `blocks` CTAs (= tickets)
 using WaveLaunch = cudaError_t (*)(const WaveArgs&, int blocks, cudaStream_t);
 // resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
 using LevelOccupancy = int (*)();

@@ -42,8 +42,18 @@ struct dwt2d_plan {
   bool generic = false;
   mutable std::once_flag dev_once;
   mutable dwt2d_b200::gpu::TapDesc* d_taps = nullptr;
+  // wavefront ticket lists (device), one per pyramid geometry
+  struct WaveSchedule {
+    std::vector<long long> key;
+    unsigned long long* d = nullptr;
+    int n = 0;
+  };
+  mutable std::mutex wave_mu;
+  mutable std::vector<WaveSchedule> wave_cache;
   ~dwt2d_plan() {
     if (d_taps) cudaFree(d_taps);
+    for (WaveSchedule& w : wave_cache)
+      if (w.d) cudaFree(w.d);
   }
 };
 
@@ -383,12 +393,26 @@ void record(void* ev, cudaStream_t st) {
   cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, flags), "event record");
 }
 
-// The wavefront kernel runs the whole pyramid when every level can take the
-// vector path (sides divisible by 4 * 2^levels for CW = 4, aligned buffers).
-// DWT2D_WAVEFRONT=0 selects one launch per level.
-bool wavefront_enabled() {
+// DWT2D_WAVEFRONT=1 runs the whole pyramid as one wavefront launch when
+// every level can take the vector path (sides divisible by 4 * 2^levels for
+// CW = 4, aligned buffers). Off by default: measured on B200 it is 3 % slower
+// than one launch per level at 16384^2: level-1 work items
+// take ~70 us, so the LL_1 rows a level-2 item reads were written too long
+// before to still be in L2, and interleaving the levels costs level 1 more
+// than it saves on the deep levels.
+// DWT2D_WAVE_FROM=k runs levels k..L as one wavefront launch after one
+// launch per level for levels 1..k-1 (the deep levels are latency bound: as
+// a wavefront, level l + 1 starts on the first LL_l rows instead of after
+// the last one).
+int wave_first_level(int levels) {
   const char* env = std::getenv("DWT2D_WAVEFRONT");
-  return !(env && *env == '0');
+  if (env && *env == '1') return 1;
+  if (env && *env == '0') return 0;
+  if (const char* f = std::getenv("DWT2D_WAVE_FROM")) {
+    const int k = std::atoi(f);
+    return k >= 1 && k < levels ? k : 0;
+  }
+  return 0;
 }
 
 // Rows per work item of level l inside the wavefront (DWT2D_WAVE_CHUNK_ROWS
@@ -397,7 +421,7 @@ bool wavefront_enabled() {
 // stays short.
 int wave_chunk_rows(const dwt2d_plan& p, int l, int h2, int nstrips) {
   if (l == 1) return chunk_rows_for(p, h2, nstrips);
-  int v = 16;
+  int v = 4;
   if (const char* env = std::getenv("DWT2D_WAVE_CHUNK_ROWS")) v = std::max(1, std::atoi(env));
   return std::min(v, h2);
 }
@@ -416,6 +440,109 @@ void fill_forward_level(gpu::LevelArgs& a, const float* cur, size_t cur_pitch, f
   a.w2 = w2, a.h2 = h2;
 }
 
+// Host mirror of level_engine.cuh: wave_deps (same formula).
+void wave_deps(const gpu::LevelArgs& a, const gpu::LevelArgs& prev, int U, int L, int c, int& lo0, int& hi0,
+               int& lo1, int& hi1) {
+  const int y0 = c * a.chunk_rows, y1 = std::min(a.h2, y0 + a.chunk_rows);
+  const int n = prev.h2;
+  const int span = 2 * (y1 - 1 + L) + 1 - 2 * (y0 - U);
+  lo1 = 1, hi1 = 0;
+  if (span + 1 >= n) {
+    lo0 = 0, hi0 = prev.nchunks - 1;
+    return;
+  }
+  const int r0 = ((2 * (y0 - U)) % n + n) % n, r1 = r0 + span;
+  if (r1 < n) {
+    lo0 = r0 / prev.chunk_rows, hi0 = r1 / prev.chunk_rows;
+  } else {
+    lo0 = r0 / prev.chunk_rows, hi0 = prev.nchunks - 1;
+    lo1 = 0, hi1 = (r1 - n) / prev.chunk_rows;
+  }
+}
+
+// Ticket order of the wavefront kernel. Each level hands out its chunks as
+// n-1, 0, 1, ..., n-2 (the next level's first chunk wraps onto the last
+// one), every chunk as consecutive tickets of kWarpsPerCta strips. Level-1 chunks are
+// appended one by one; before each, every deeper level appends the chunks
+// whose inputs were appended at least `lag` tickets earlier (about one wave
+// of resident CTAs: they are then finished, or nearly, when a CTA takes
+// the dependent ticket). When level 1 is exhausted the remaining deep chunks
+// follow in dependency order. Every ticket comes after all tickets it
+// depends on, which is what makes the kernel's waits deadlock-free.
+std::vector<unsigned long long> wave_schedule(const std::vector<gpu::LevelArgs>& lv, int U, int L, long long lag) {
+  const int n = int(lv.size());
+  std::vector<std::vector<long long>> end(n);
+  for (int l = 0; l < n; ++l) end[l].assign(size_t(lv[l].nchunks), -1);
+  std::vector<int> pos(n, 0);
+  std::vector<unsigned long long> out;
+  auto chunk_at = [&](int l, int p) { return p == 0 ? lv[l].nchunks - 1 : p - 1; };
+  auto ready = [&](int l, long long need_lag) {
+    if (pos[l] >= lv[l].nchunks) return false;
+    int lo0, hi0, lo1, hi1;
+    wave_deps(lv[l], lv[l - 1], U, L, chunk_at(l, pos[l]), lo0, hi0, lo1, hi1);
+    const long long now = (long long)out.size();
+    for (int r = 0; r < 2; ++r)
+      for (int d = r ? lo1 : lo0; d <= (r ? hi1 : hi0); ++d) {
+        const long long e = end[l - 1][size_t(d)];
+        if (e < 0 || now - e < need_lag) return false;
+      }
+    return true;
+  };
+  auto emit = [&](int l) {
+    const int c = chunk_at(l, pos[l]);
+    const int groups = (lv[l].nstrips + gpu::kWarpsPerCta - 1) / gpu::kWarpsPerCta;
+    for (int g = 0; g < groups; ++g)
+      out.push_back((static_cast<unsigned long long>(l) << 56) | (static_cast<unsigned long long>(g) << 32) |
+                    static_cast<unsigned long long>(unsigned(c)));
+    end[l][size_t(c)] = (long long)out.size();
+    ++pos[l];
+  };
+  while (pos[0] < lv[0].nchunks) {
+    for (int l = n - 1; l >= 1; --l)
+      while (ready(l, lag)) emit(l);
+    emit(0);
+  }
+  for (bool more = true; more;) {
+    more = false;
+    for (int l = 1; l < n; ++l)
+      while (ready(l, 0)) emit(l), more = true;
+  }
+  for (int l = 0; l < n; ++l)
+    if (pos[l] != lv[l].nchunks) fail(DWT2D_ECUDA, "wavefront schedule incomplete");
+  return out;
+}
+
+// Device copy of the ticket list for this geometry, built and uploaded on
+// first use. Returns null (caller falls back to one launch per level) when
+// the stream is being captured and the list does not exist yet: a
+// synchronous upload cannot be captured.
+const unsigned long long* wave_tickets(const dwt2d_plan& p, const std::vector<gpu::LevelArgs>& lv, long long lag,
+                                       cudaStream_t st, int& ntickets) {
+  std::vector<long long> key{lag};
+  for (const gpu::LevelArgs& a : lv) key.insert(key.end(), {a.w2, a.h2, a.chunk_rows, a.nstrips});
+  std::lock_guard<std::mutex> lk(p.wave_mu);
+  for (const dwt2d_plan::WaveSchedule& w : p.wave_cache)
+    if (w.key == key) {
+      ntickets = w.n;
+      return w.d;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cs), "capture status");
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  const std::vector<unsigned long long> t = wave_schedule(lv, p.entry->up, p.entry->down, lag);
+  dwt2d_plan::WaveSchedule w;
+  w.key = key;
+  w.n = int(t.size());
+  void* d = nullptr;
+  cuda_check(cudaMalloc(&d, t.size() * sizeof(unsigned long long)), "wavefront ticket allocation");
+  w.d = static_cast<unsigned long long*>(d);
+  cuda_check(cudaMemcpy(w.d, t.data(), t.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice),
+             "wavefront ticket upload");
+  p.wave_cache.push_back(std::move(w));
+  ntickets = p.wave_cache.back().n;
+  return p.wave_cache.back().d;
+}
+
 void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W, int H, int levels,
                     float* out, size_t out_pitch, float* ws, cudaStream_t st,
                     void* const* events = nullptr) {
@@ -431,16 +558,22 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     cur = ll;
     cur_pitch = ll_pitch;
   }
-  bool wave = p.entry && p.entry->wave && levels >= 2 && levels <= gpu::kMaxWaveLevels && wavefront_enabled();
+  // levels first..levels run as one wavefront launch (first = 0: none)
+  int first = wave_first_level(levels);
+  bool wave = first > 0 && p.entry && p.entry->wave && levels - first + 1 >= 2 &&
+              levels - first + 1 <= gpu::kMaxWaveLevels;
+  std::vector<gpu::LevelArgs> wl;
   if (wave) {
-    for (int l = 1; l <= levels && wave; ++l) {
-      gpu::LevelArgs& a = lv[l - 1];
+    for (int l = first; l <= levels && wave; ++l) {
+      gpu::LevelArgs a = lv[l - 1];
       prepare(p, a, kFromImage);
       const int nstrips = a.nstrips;
       prepare(p, a, kFromImage, wave_chunk_rows(p, l, a.h2, nstrips));
       wave = wave && a.vec;
+      wl.push_back(a);
     }
   }
+  gpu::WaveArgs t{};
   if (wave) {
     static thread_local const gpu::PlanEntry* cached = nullptr;
     static thread_local int per_sm = 0;
@@ -449,31 +582,53 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
       per_sm = p.entry->wave_occupancy ? p.entry->wave_occupancy() : 0;
     }
     if (per_sm <= 0) fail(DWT2D_ECUDA, "wavefront kernel cannot be resident");
-    gpu::WaveArgs t{};
-    t.nlev = levels;
-    t.state = reinterpret_cast<unsigned*>(ws + ll_offset(W, H, levels));
-    int off = levels;
-    for (int l = 0; l < levels; ++l) {
-      t.lv[l] = lv[l];
-      t.done_off[l] = off;
-      off += lv[l].nchunks;
-    }
-    cuda_check(cudaMemsetAsync(t.state, 0, size_t(off) * sizeof(unsigned), st), "wavefront counters");
-    cuda_check(p.entry->wave(t, per_sm * sm_count(), st), "wavefront kernel launch");
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (events)
-      for (int l = 1; l <= levels; ++l) record(events[l], st);
-    return;
+    const int blocks = per_sm * sm_count();
+    double lag_waves = first == 1 ? 1.5 : 0.0;
+    if (const char* env = std::getenv("DWT2D_WAVE_LAG")) lag_waves = std::atof(env);
+    const long long lag = (long long)(lag_waves * blocks);
+    t.tickets = wave_tickets(p, wl, lag, st, t.ntickets);
+    wave = t.tickets != nullptr;
   }
-  for (int l = 1; l <= levels; ++l) {
+  const int last_single = wave ? first - 1 : levels;
+  // tuning: DWT2D_LEVEL_CHUNK_ROWS="r1,r2,..." overrides the chunk rows of
+  // the per-level launches (0 or missing entries keep the policy)
+  std::vector<int> level_chunks;
+  if (const char* env = std::getenv("DWT2D_LEVEL_CHUNK_ROWS"))
+    for (const char* q = env; *q;) {
+      level_chunks.push_back(std::atoi(q));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+  for (int l = 1; l <= last_single; ++l) {
     gpu::LevelArgs a = lv[l - 1];
     // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
     // level l wrote last, which are still in L2 (LL uses normal stores, the
     // detail bands evict-first).
     a.reverse = (l % 2 == 0) ? 1 : 0;
+    if (l - 1 < int(level_chunks.size()) && level_chunks[l - 1] > 0 && p.entry) {
+      prepare(p, a, kFromImage, level_chunks[l - 1]);
+      cuda_check((*p.entry->from_image)(a, st), "level kernel launch");
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (events) record(events[l], st);
+      continue;
+    }
     launch(p, a, kFromImage, st);
     if (events) record(events[l], st);
   }
+  if (!wave) return;
+  t.nlev = int(wl.size());
+  t.state = reinterpret_cast<unsigned*>(ws + ll_offset(W, H, levels));
+  int off = 1;
+  for (int l = 0; l < t.nlev; ++l) {
+    t.lv[l] = wl[l];
+    t.done_off[l] = off;
+    off += wl[l].nchunks;
+  }
+  cuda_check(cudaMemsetAsync(t.state, 0, size_t(off) * sizeof(unsigned), st), "wavefront counters");
+  cuda_check(p.entry->wave(t, t.ntickets, st), "wavefront kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (events)
+    for (int l = first; l <= levels; ++l) record(events[l], st);
 }
 
 void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W, int H, int levels,

@@ -211,6 +211,27 @@ def test_wavefront_pyramid_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
         assert torch.equal(a, b), (W, H, L, c1, cd)
 
 
+@pytest.mark.parametrize("first", [2, 3, 5])
+def test_deep_level_wavefront_bit_exact(dwt, cuda, first, monkeypatch):
+    """Levels 1..first-1 one launch each, levels first..L as one wavefront:
+    same bits as one launch per level, and first-1 + 1 launches."""
+    import torch
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
+    W, H, L = 2048, 1024, 7
+    img = torch.from_numpy(O.random_image(W, H, 3)).to(cuda)
+    monkeypatch.setenv("DWT2D_WAVEFRONT", "0")
+    a = plan.forward_mallat(img, L)
+    monkeypatch.delenv("DWT2D_WAVEFRONT")
+    monkeypatch.setenv("DWT2D_WAVE_FROM", str(first))
+    for cd in ["1", "2", "4", "7"]:
+        monkeypatch.setenv("DWT2D_WAVE_CHUNK_ROWS", cd)
+        before = dwt.launch_count()
+        b = plan.forward_mallat(img, L)
+        torch.cuda.synchronize()
+        assert dwt.launch_count() - before == first, cd
+        assert torch.equal(a, b), (first, cd)
+
+
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-convolution", False),
                                      ("dd137", "nonseparable-lifting", False), ("cdf53", "inverse-lifting", False)])
 def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
@@ -288,6 +309,7 @@ def test_launch_count_and_native_library_loaded(dwt, cuda, monkeypatch):
     plan.forward_mallat(img, 8)  # level 8 is 1 component wide: no vector path, one launch per level
     torch.cuda.synchronize()
     assert dwt.launch_count() - before == 8
+    monkeypatch.setenv("DWT2D_WAVEFRONT", "1")
     before = dwt.launch_count()
     plan.forward_mallat(img, 6)  # wavefront: all levels in one launch
     torch.cuda.synchronize()
