@@ -201,18 +201,29 @@ def run_single(args, plan, img, out, dev):
         return g
 
     timed_events = [[Event(), Event()] + [None] * (LEVELS - 1) for _ in range(args.steps)]
-    launches0 = dwt.launch_count()
-    graph = capture(timed_events)
-    launches = dwt.launch_count() - launches0
-    with torch.cuda.stream(stream):
-        graph.replay()  # untimed replay warms the graph
-    torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
-        t0.record(stream)
-        graph.replay()  # replays on the current stream (= `stream` here)
-        t1.record(stream)
-        t1.synchronize()
+    if args.launch == "graph":
+        launches0 = dwt.launch_count()
+        graph = capture(timed_events)
+        launches = dwt.launch_count() - launches0
+        with torch.cuda.stream(stream):
+            graph.replay()  # untimed replay warms the graph
+        torch.cuda.synchronize()
+        with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
+            t0.record(stream)
+            graph.replay()  # replays on the current stream (= `stream` here)
+            t1.record(stream)
+            t1.synchronize()
+    else:  # eager: the library's calls as a user makes them (levels chained by PDL)
+        torch.cuda.synchronize()
+        launches0 = dwt.launch_count()
+        with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
+            t0.record(stream)
+            for evs in timed_events:
+                step(evs)
+            t1.record(stream)
+            t1.synchronize()
+        launches = dwt.launch_count() - launches0
     torch.cuda.synchronize()
     ms_per_step = t0.elapsed_time(t1) / args.steps
     level1_ms = statistics.mean(e[0].elapsed_ms(e[1]) for e in timed_events)
@@ -281,6 +292,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
+                    help="timed region: one CUDA graph of K pyramids, or K eager library calls")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

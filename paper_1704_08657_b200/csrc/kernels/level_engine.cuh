@@ -519,6 +519,11 @@ __device__ __forceinline__ void level_dispatch(const LevelArgs& a, const int wid
 template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, int MIN_CTAS = 1>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
 level_kernel(const LevelArgs a) {
+  // PDL (registry.hpp: launch_level): the previous kernel's results are
+  // visible after the wait; the next launch may begin once every CTA of this
+  // grid has started. Both are no-ops for a normal launch.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
   level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC>(a, wid);

@@ -16,16 +16,28 @@ namespace gpu {
 
 constexpr int kPrefetchRows = 2;
 
+// Level launches use programmatic dependent launch (PDL): the kernel waits
+// for the previous kernel in the stream (griddepcontrol.wait) before it
+// reads anything and lets the next one launch once all its own CTAs have
+// started, so consecutive levels overlap launch latency and CTA ramp-up with
+// the previous level's last wave. DWT2D_PDL=0 disables it.
+bool pdl_enabled();
+
 template <class P, bool IN_IL, bool OUT_IL>
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   const long long warps = (long long)a.nstrips * a.nchunks;
   if (warps <= 0) return cudaSuccess;
-  const unsigned blocks = unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta);
-  if (a.vec)
-    level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true><<<blocks, kWarpsPerCta * 32, 0, st>>>(a);
-  else
-    level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, false><<<blocks, kWarpsPerCta * 32, 0, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta));
+  cfg.blockDim = dim3(kWarpsPerCta * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (a.vec) return cudaLaunchKernelEx(&cfg, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true>, a);
+  return cudaLaunchKernelEx(&cfg, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, false>, a);
 }
 
 template <class P, bool IN_IL, bool OUT_IL>

@@ -23,6 +23,15 @@
 
 using namespace dwt2d_b200;
 
+namespace dwt2d_b200 {
+namespace gpu {
+bool pdl_enabled() {
+  const char* env = std::getenv("DWT2D_PDL");
+  return !(env && *env == '0');
+}
+}  // namespace gpu
+}  // namespace dwt2d_b200
+
 struct dwt2d_plan {
   std::string key;
   std::uint64_t fingerprint = 0;
