@@ -6,7 +6,9 @@
 // reflects every intermediate, incompatible with one streaming pass) and
 // definition-file wavelets of new shapes. Same accumulation order and
 // rounding as the fused kernels, so periodic results are bit-identical to
-// them and composed results to the reference's float32 executor.
+// them and composed results to the reference's float32 executor. One launch
+// can run the same sub-step over up to four grids (the border crops of the
+// symmetric path, capi.cpp: run_symmetric).
 #include <cuda_runtime.h>
 
 #include "level_types.hpp"
@@ -34,10 +36,15 @@ __device__ __forceinline__ float load(const GenericStepArgs& a, int j, int x, in
   return a.in[j][(long long)y * a.in_pitch[j] + x];
 }
 
-__global__ void __launch_bounds__(256) generic_step_kernel(const GenericStepArgs a) {
+struct GenericBatch {
+  GenericStepArgs r[kMaxGenericRegions];
+};
+
+__global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant__ GenericBatch b) {
+  const GenericStepArgs& a = b.r[blockIdx.z];
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  if (x >= a.w2 || y >= a.h2) return;
+  if (x < a.kx0 || x >= a.kx1 || y < a.ky0 || y >= a.ky1) return;
   for (int r = 0; r < 4; ++r) {
     float v;
     if (a.rows[r].ident) {
@@ -65,10 +72,18 @@ __global__ void __launch_bounds__(256) generic_step_kernel(const GenericStepArgs
 
 }  // namespace
 
-cudaError_t launch_generic_step(const GenericStepArgs& a, cudaStream_t st) {
+cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st) {
+  if (n < 1 || n > kMaxGenericRegions) return cudaErrorInvalidValue;
+  GenericBatch b{};
+  int w = 0, h = 0;
+  for (int i = 0; i < n; ++i) {
+    b.r[i] = a[i];
+    w = w > a[i].w2 ? w : a[i].w2;
+    h = h > a[i].h2 ? h : a[i].h2;
+  }
   const dim3 block(32, 8);
-  const dim3 grid((a.w2 + 31) / 32, (a.h2 + 7) / 8);
-  generic_step_kernel<<<grid, block, 0, st>>>(a);
+  const dim3 grid((w + 31) / 32, (h + 7) / 8, n);
+  generic_step_kernel<<<grid, block, 0, st>>>(b);
   return cudaGetLastError();
 }
 

@@ -526,7 +526,7 @@ level_kernel(const LevelArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC>(a, wid);
+  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && P::kAlt>(a, wid);
 }
 
 // ------------------------------------------------ wavefront pyramid kernel
@@ -612,10 +612,15 @@ wave_kernel(const __grid_constant__ WaveArgs t) {
       __nanosleep(200);
     }
   }
-  if (a.alternate && (chunk & 1))
-    level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
-  else
+  if constexpr (P::kAlt) {
+    if (a.alternate && (chunk & 1)) {
+      level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
+    } else {
+      level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
+    }
+  } else {
     level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
+  }
   __threadfence();
   __syncwarp();
   if (lane == 0) atomicAdd(t.state + t.done_off[lvl] + chunk, 1u);

@@ -95,13 +95,17 @@ struct GenericStepArgs {
   float* out[4];
   long long out_pitch[4];
   int out_il;            // out[0] is an interleaved image
-  int w2, h2;
+  int w2, h2;            // grid of this pass (a whole level, or a crop of it)
   int symmetric;         // extend_index rule on the component grid
   int fma;               // rounding model (see lowering.hpp)
+  int kx0, kx1, ky0, ky1;  // outputs written only inside this window
   RowDesc rows[4];
   const TapDesc* taps;
 };
-cudaError_t launch_generic_step(const GenericStepArgs& a, cudaStream_t st);
+// up to kMaxGenericRegions independent passes (same sub-step, different
+// grids) in one launch
+constexpr int kMaxGenericRegions = 4;
+cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st);
 
 const std::vector<PlanEntry>& plan_registry();
 const PlanEntry* find_plan(unsigned long long fingerprint);

@@ -132,18 +132,23 @@ bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(
 // span the whole image; 8192^2 inside the pyramid: 106 us with 16-row
 // chunks vs 113 us with one wave of 81-row chunks); tiny L2-resident levels
 // want the most warps (2-row chunks).
-int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
-  if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
-    const int v = std::atoi(env);
-    if (v > 0) return v;
-  }
+// warps of the plan's vector level kernel that are resident at once
+long long resident_warps(const dwt2d_plan& p) {
   static thread_local const gpu::PlanEntry* cached_entry = nullptr;
   static thread_local int cached_blocks = 0;
   if (cached_entry != p.entry) {
     cached_entry = p.entry;
     cached_blocks = p.entry->occupancy ? p.entry->occupancy() : 0;
   }
-  const long long resident = std::max(1, cached_blocks ? cached_blocks : 2) * 4ll * sm_count();
+  return std::max(1, cached_blocks ? cached_blocks : 2) * (long long)gpu::kWarpsPerCta * sm_count();
+}
+
+int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
+  if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
+    const int v = std::atoi(env);
+    if (v > 0) return v;
+  }
+  const long long resident = resident_warps(p);
   const long long rows_total = (long long)h2 * std::max(1, nstrips);
   const long long per_warp = (rows_total + resident - 1) / resident;
   long long chunk = per_warp <= 48 ? std::max<long long>(2, per_warp)
@@ -154,19 +159,25 @@ int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
 enum Layout { kPlanar, kFromImage, kToImage };
 
 // Work decomposition and vector-path eligibility of one level launch.
-bool alternate_chunks() {
+int alternate_chunks() {
   const char* env = std::getenv("DWT2D_ALTERNATE");
-  return !(env && *env == '0');
+  if (env && *env == '0') return 0;
+  return env && *env == '2' ? 2 : 1;  // 2: also single-wave levels (tests)
 }
 
 void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_override = 0) {
   if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
-  a.alternate = alternate_chunks() ? 1 : 0;
+  a.alternate = alternate_chunks();
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
   a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, a.h2) : chunk_rows_for(p, a.h2, a.nstrips);
   a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
+  // bottom-up odd chunks pay once the level streams from HBM (their shared
+  // warm-up rows then meet in L2: 4096^2 single level 30.7 vs 32.8 us); a
+  // level whose input (16 B per quad) fits comfortably in L2 streams
+  // top-down (1024^2 round trip 27.7 vs 33.8 us)
+  if (a.alternate == 1 && size_t(a.w2) * size_t(a.h2) * 16 < (size_t(32) << 20)) a.alternate = 0;
   bool vec = a.w2 % cw == 0;
   const bool in_il = layout == kFromImage, out_il = layout == kToImage;
   for (int j = 0; j < 4; ++j) {
@@ -214,46 +225,124 @@ const gpu::TapDesc* device_taps(const dwt2d_plan& p) {
   return p.d_taps;
 }
 
+size_t ws_align(size_t floats) { return (floats + 63) & ~size_t(63); }
+
+// A sub-grid of a level for the generic executor: the crop [x0, x0 + w) x
+// [y0, y0 + h) of the component grid is transformed as if it were the whole
+// image (extension at the crop's edges); only outputs inside the keep window
+// (crop coordinates) are written.
+struct Region {
+  int x0, y0, w, h;
+  int kx0, kx1, ky0, ky1;
+};
+
 // One level on the generic executor: sub-step s reads the previous
-// sub-step's planes (double-buffered temporaries), like the reference's run().
-void run_generic(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+// sub-step's planes (double-buffered temporaries per region), like the
+// reference's run(); all regions of a sub-step go in one launch.
+void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout,
+                         const std::vector<Region>& regions, cudaStream_t st) {
   if (a.halo) fail(DWT2D_EUNSUPPORTED, "row strips need a fused kernel (periodic built-in program)");
+  if (regions.empty() || int(regions.size()) > gpu::kMaxGenericRegions) fail(DWT2D_EINVAL, "generic regions");
   keep_pool_memory();
   const gpu::TapDesc* taps = device_taps(p);
   const int S = p.substeps;
-  const size_t plane = size_t(a.w2) * size_t(a.h2);
+  const int n = int(regions.size());
+  std::vector<size_t> off(n + 1, 0);  // per region: 2 buffers x 4 planes
+  for (int i = 0; i < n; ++i) off[i + 1] = off[i] + ws_align(size_t(regions[i].w) * size_t(regions[i].h)) * 8;
   float* tmp = nullptr;
   if (S > 1) {
     void* m = nullptr;
-    cuda_check(cudaMallocAsync(&m, (S > 2 ? 8 : 4) * plane * sizeof(float), st), "generic temporaries");
+    cuda_check(cudaMallocAsync(&m, off[n] * sizeof(float), st), "generic temporaries");
     tmp = static_cast<float*>(m);
   }
+  std::vector<gpu::GenericStepArgs> g(n);
   for (int s = 0; s < S; ++s) {
-    gpu::GenericStepArgs g{};
     const bool first = s == 0, last = s == S - 1;
-    float* src_tmp = tmp + size_t((s - 1) % 2) * 4 * plane;
-    float* dst_tmp = tmp + size_t(s % 2) * 4 * plane;
-    for (int j = 0; j < 4; ++j) {
-      g.in[j] = first ? a.in[j] : src_tmp + j * plane;
-      g.in_pitch[j] = first ? a.in_pitch[j] : a.w2;
-      g.out[j] = last ? a.out[j] : dst_tmp + j * plane;
-      g.out_pitch[j] = last ? a.out_pitch[j] : a.w2;
-      const dwt2d_row& r = p.rows[size_t(s) * 4 + j];
-      g.rows[j] = gpu::RowDesc{r.identity, r.tap_begin, r.tap_end, r.scale};
+    for (int i = 0; i < n; ++i) {
+      const Region& r = regions[i];
+      const size_t plane = ws_align(size_t(r.w) * size_t(r.h));
+      float* src_tmp = tmp ? tmp + off[i] + size_t((s + 1) % 2) * 4 * plane : nullptr;
+      float* dst_tmp = tmp ? tmp + off[i] + size_t(s % 2) * 4 * plane : nullptr;
+      gpu::GenericStepArgs& q = g[i];
+      q = gpu::GenericStepArgs{};
+      for (int j = 0; j < 4; ++j) {
+        if (first) {
+          q.in[j] = layout == kFromImage
+                        ? a.in[0] + 2ll * r.y0 * a.in_pitch[0] + 2ll * r.x0
+                        : a.in[j] + (long long)r.y0 * a.in_pitch[j] + r.x0;
+          q.in_pitch[j] = a.in_pitch[layout == kFromImage ? 0 : j];
+        } else {
+          q.in[j] = src_tmp + j * plane;
+          q.in_pitch[j] = r.w;
+        }
+        if (last) {
+          q.out[j] = layout == kToImage ? a.out[0] + 2ll * r.y0 * a.out_pitch[0] + 2ll * r.x0
+                                        : a.out[j] + (long long)r.y0 * a.out_pitch[j] + r.x0;
+          q.out_pitch[j] = a.out_pitch[layout == kToImage ? 0 : j];
+        } else {
+          q.out[j] = dst_tmp + j * plane;
+          q.out_pitch[j] = r.w;
+        }
+        const dwt2d_row& row = p.rows[size_t(s) * 4 + j];
+        q.rows[j] = gpu::RowDesc{row.identity, row.tap_begin, row.tap_end, row.scale};
+      }
+      q.in_il = first && layout == kFromImage;
+      q.out_il = last && layout == kToImage;
+      q.w2 = r.w, q.h2 = r.h;
+      q.symmetric = p.extension == DWT2D_SYMMETRIC;
+      q.fma = p.fma;
+      if (last)
+        q.kx0 = r.kx0, q.kx1 = r.kx1, q.ky0 = r.ky0, q.ky1 = r.ky1;
+      else
+        q.kx0 = 0, q.kx1 = r.w, q.ky0 = 0, q.ky1 = r.h;
+      q.taps = taps;
     }
-    g.in_il = first && layout == kFromImage;
-    g.out_il = last && layout == kToImage;
-    g.w2 = a.w2, g.h2 = a.h2;
-    g.symmetric = p.extension == DWT2D_SYMMETRIC;
-    g.fma = p.fma;
-    g.taps = taps;
-    cuda_check(gpu::launch_generic_step(g, st), "generic step launch");
+    cuda_check(gpu::launch_generic_step(g.data(), n, st), "generic step launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (tmp) cuda_check(cudaFreeAsync(tmp, st), "generic temporaries");
 }
 
+void run_generic(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+  run_generic_regions(p, a, layout, {Region{0, 0, a.w2, a.h2, 0, a.w2, 0, a.h2}}, st);
+}
+
+void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st);
+
+// Symmetric extension with a fused kernel. The extension
+// only matters for outputs whose dependency cone — the level's reach, up/down
+// rows and left/right columns over all sub-steps — crosses the image edge;
+// everywhere else the fused single-pass kernel (periodic input rule) computes
+// the same taps in the same order, i.e. the same bits as the per-step
+// symmetric executor. So: the fused kernel over the whole level, then the
+// four border bands recomputed by the generic executor on crops that contain
+// the true image edge plus a margin (a cone that reflects at the true edge
+// reaches at most up + down rows, resp. left + right columns, into the crop;
+// the margin keeps the crop's artificial inner edge out of every kept
+// cone). Levels too small for the crops run wholly on the generic executor.
+void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+  const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
+  if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
+  launch_fused(p, a, layout, st);
+  const int w2 = a.w2, h2 = a.h2;
+  run_generic_regions(p, a, layout,
+                      {Region{0, 0, w2, my, 0, w2, 0, p.up},
+                       Region{0, h2 - my, w2, my, 0, w2, my - p.down, my},
+                       Region{0, 0, mx, h2, 0, p.left, 0, h2},
+                       Region{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2}},
+                      st);
+}
+
 void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
+  if (!p.generic && p.extension == DWT2D_SYMMETRIC) {
+    if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    if (a.halo) fail(DWT2D_EUNSUPPORTED, "row strips need periodic extension");
+    return run_symmetric(p, a, layout, st);
+  }
+  launch_fused(p, a, layout, st);
+}
+
+void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
   if (p.generic) {
     if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
     if (layout != kPlanar && (layout == kToImage) == (p.forward != 0))
@@ -301,11 +390,12 @@ void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) identity = identity && r.identity;
   if (identity) return;  // pure copy, no kernel (pairless wavelet)
-  // the fused single-pass kernels cover periodic extension of the built-in
-  // programs; everything else runs on the generic GPU executor (one pass per
-  // sub-step, kernels/generic_step.cu)
+  // the fused single-pass kernels cover the built-in programs (symmetric
+  // extension: plus border crops on the generic executor, run_symmetric);
+  // everything else runs on the generic GPU executor (one pass per sub-step,
+  // kernels/generic_step.cu)
   const char* force = std::getenv("DWT2D_FORCE_GENERIC");  // testing: bypass the fused kernels
-  const bool fused_ok = extension == DWT2D_PERIODIC && !(force && *force && *force != '0');
+  const bool fused_ok = !(force && *force && *force != '0');
   p.entry = fused_ok ? gpu::find_plan(p.fingerprint) : nullptr;
   p.generic = p.entry == nullptr;
 }
@@ -362,7 +452,6 @@ void check_pyramid(int W, int H, int levels) {
 // Workspace layout (dwt2d_workspace_bytes): the intermediate LL band of every
 // level k = 1 .. levels-1 in its own slot (the wavefront kernel has all levels
 // in flight at once), then the wavefront's scheduling counters.
-size_t ws_align(size_t floats) { return (floats + 63) & ~size_t(63); }
 size_t ll_offset(int W, int H, int k) {
   size_t off = 0;
   for (int i = 1; i < k; ++i) off += ws_align(size_t(W >> i) * size_t(H >> i));
@@ -569,7 +658,7 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
   }
   // levels first..levels run as one wavefront launch (first = 0: none)
   int first = wave_first_level(levels);
-  bool wave = first > 0 && p.entry && p.entry->wave && levels - first + 1 >= 2 &&
+  bool wave = first > 0 && p.entry && p.entry->wave && p.extension == DWT2D_PERIODIC && levels - first + 1 >= 2 &&
               levels - first + 1 <= gpu::kMaxWaveLevels;
   std::vector<gpu::LevelArgs> wl;
   if (wave) {
@@ -614,7 +703,7 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     // level l wrote last, which are still in L2 (LL uses normal stores, the
     // detail bands evict-first).
     a.reverse = (l % 2 == 0) ? 1 : 0;
-    if (l - 1 < int(level_chunks.size()) && level_chunks[l - 1] > 0 && p.entry) {
+    if (l - 1 < int(level_chunks.size()) && level_chunks[l - 1] > 0 && p.entry && p.extension == DWT2D_PERIODIC) {
       prepare(p, a, kFromImage, level_chunks[l - 1]);
       cuda_check((*p.entry->from_image)(a, st), "level kernel launch");
       g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1157,7 +1246,7 @@ int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, in
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
     if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
-    if (p->entry) {
+    if (p->entry && p->extension == DWT2D_PERIODIC) {
       forward_mallat_host_pipelined(*p, image, W, H, levels, out);
     } else {
       HostPipe& hp = host_pipe();

@@ -119,6 +119,27 @@ def main():
                   "gpu_ms_median": med, "gpu_ms_min": mn, "gpu_gpix_s": W * H / (med * 1e-3) / 1e9,
                   "gpu_gbs": gbs(W, H, med), "frac_of_measured_copy": gbs(W, H, med) / peak})
 
+    # symmetric extension: fused kernel + generic border
+    # crops vs the all-generic per-step executor, headline scheme
+    for n, levels in ((4096, 1), (16384, 8)):
+        img = random_image(n, n, 1, device="cuda")
+        out = torch.empty_like(img)
+        res = {}
+        for mode in ("fused", "generic"):
+            if mode == "generic":
+                os.environ["DWT2D_FORCE_GENERIC"] = "1"
+            plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+            os.environ.pop("DWT2D_FORCE_GENERIC", None)
+            plan.forward_mallat(img, levels, out=out)
+            res[mode] = timed(lambda: plan.forward_mallat(img, levels, out=out), max(5, reps // 4))
+        emit({"config": "symmetric", "workload": f"cdf97 nonseparable-lifting (optimized) symmetric extension "
+                                                 f"{n}^2, {levels} level(s)",
+              "gpu_ms_median": res["fused"][0], "gpu_ms_min": res["fused"][1],
+              "gpu_gpix_s": n * n / (res["fused"][0] * 1e-3) / 1e9,
+              "gpu_gbs": gbs(n, n, res["fused"][0], levels),
+              "generic_executor_ms_median": res["generic"][0]})
+        del img, out
+
     # configs[2]
     fwd = dwt.Plan("cdf97", "nonseparable-polyconvolution", optimized=True)
     inv = dwt.Plan("cdf97", "inverse-lifting")

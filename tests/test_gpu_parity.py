@@ -232,8 +232,8 @@ def test_deep_level_wavefront_bit_exact(dwt, cuda, first, monkeypatch):
         assert torch.equal(a, b), (first, cd)
 
 
-@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-convolution", False),
-                                     ("dd137", "nonseparable-lifting", False), ("cdf53", "inverse-lifting", False)])
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-lifting", False),
+                                     ("dd137", "nonseparable-lifting", True), ("cdf53", "inverse-lifting", False)])
 def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     """Odd chunks streaming bottom-up (DWT2D_ALTERNATE) produce the same bits
     as all-top-down streaming, for several chunk sizes incl. ragged ones."""
@@ -246,7 +246,7 @@ def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
         monkeypatch.setenv("DWT2D_ALTERNATE", "0")
         a = plan.run(planes)
         fa = plan.forward_level(img) if s != "inverse-lifting" else a
-        monkeypatch.setenv("DWT2D_ALTERNATE", "1")
+        monkeypatch.setenv("DWT2D_ALTERNATE", "2")  # also on this single-wave level
         b = plan.run(planes)
         fb = plan.forward_level(img) if s != "inverse-lifting" else b
         for j in range(4):
@@ -363,6 +363,51 @@ def test_symmetric_reconstruction(dwt, cuda, w):
         sl = (slice(margin, -margin or None), slice(margin, -margin or None))
         e = max(float((b[sl] - p[sl]).abs().max()) for b, p in zip(back, planes))
         assert e <= 5e-5 * (8 if w == "dd137" else 1), (s, e)
+
+
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-convolution", False),
+                                     ("cdf53", "nonseparable-polyconvolution", True),
+                                     ("dd137", "nonseparable-lifting", False), ("cdf97", "inverse-lifting", False),
+                                     ("dd137", "separable-lifting", True)])
+def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+    """Symmetric extension on the fused kernel + generic border crops equals
+    the all-generic per-step symmetric executor bit for bit: planar run(),
+    forward level from the image, inverse level to the image, incl. odd
+    (scalar-path) widths and grids just above the crop threshold."""
+    import torch
+    fused = dwt.Plan(w, s, optimized=opt, extension="symmetric")
+    monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
+    gen = dwt.Plan(w, s, optimized=opt, extension="symmetric")
+    monkeypatch.delenv("DWT2D_FORCE_GENERIC")
+    assert fused.info["generic"] == 0 and gen.info["generic"] == 1
+    for (w2, h2) in [(64, 48), (150, 101), (300, 40), (40, 300), (33, 33)]:
+        planes = _to_dev(O.split(O.random_image(2 * w2, 2 * h2, 7 + w2)), cuda)
+        a, b = fused.run(planes), gen.run(planes)
+        for j in range(4):
+            assert torch.equal(a[j], b[j]), (w2, h2, j)
+        if s == "inverse-lifting":
+            ia, ib = fused.inverse_level(planes), gen.inverse_level(planes)
+            assert torch.equal(ia, ib), (w2, h2)
+        else:
+            img = torch.from_numpy(O.random_image(2 * w2, 2 * h2, 3)).to(cuda)
+            fa, fb = fused.forward_level(img), gen.forward_level(img)
+            for j in range(4):
+                assert torch.equal(fa[j], fb[j]), (w2, h2, j)
+
+
+def test_symmetric_fused_pyramid_bit_exact(dwt, cuda, monkeypatch):
+    import torch
+    W, H, L = 1024, 768, 6
+    img = torch.from_numpy(O.random_image(W, H, 11)).to(cuda)
+    fused = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+    inv = dwt.Plan("cdf97", "inverse-lifting", extension="symmetric")
+    monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
+    gen = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+    ginv = dwt.Plan("cdf97", "inverse-lifting", extension="symmetric")
+    monkeypatch.delenv("DWT2D_FORCE_GENERIC")
+    a, b = fused.forward_mallat(img, L), gen.forward_mallat(img, L)
+    assert torch.equal(a, b)
+    assert torch.equal(inv.inverse_mallat(a, L), ginv.inverse_mallat(b, L))
 
 
 def test_symmetric_pyramid_and_inverse(dwt, cuda):

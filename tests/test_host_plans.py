@@ -150,6 +150,9 @@ def test_definition_file_wavelet(dwt, tmp_path):
         dwt.Plan(str(bad), "separable-lifting")
 
 
-def test_symmetric_plans_use_generic_executor(dwt):
+def test_symmetric_plans_use_the_fused_kernel(dwt):
+    """symmetric extension: fused kernel + generic border crops (capi.cpp:
+    run_symmetric); definition-file programs without an AOT kernel stay on
+    the generic executor"""
     p = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
-    assert p.info["generic"] == 1 and p.info["extension"] == 1
+    assert p.info["generic"] == 0 and p.info["extension"] == 1
