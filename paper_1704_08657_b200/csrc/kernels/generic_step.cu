@@ -36,14 +36,23 @@ __device__ __forceinline__ float load(const GenericStepArgs& a, int j, int x, in
   return a.in[j][(long long)y * a.in_pitch[j] + x];
 }
 
+// regions of very different shapes (full-width row bands, full-height column
+// bands) share one flat grid: region i owns blocks [first[i], first[i+1]),
+// tiles of 32 x 8 in row-major order over its grid
 struct GenericBatch {
   GenericStepArgs r[kMaxGenericRegions];
+  int first[kMaxGenericRegions + 1];
+  int tiles_x[kMaxGenericRegions];
+  int n;
 };
 
 __global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant__ GenericBatch b) {
-  const GenericStepArgs& a = b.r[blockIdx.z];
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  int i = 0;
+  while (i + 1 < b.n && int(blockIdx.x) >= b.first[i + 1]) ++i;
+  const GenericStepArgs& a = b.r[i];
+  const int tile = int(blockIdx.x) - b.first[i];
+  const int x = (tile % b.tiles_x[i]) * 32 + threadIdx.x;
+  const int y = (tile / b.tiles_x[i]) * 8 + threadIdx.y;
   if (x < a.kx0 || x >= a.kx1 || y < a.ky0 || y >= a.ky1) return;
   for (int r = 0; r < 4; ++r) {
     float v;
@@ -75,15 +84,15 @@ __global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant
 cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st) {
   if (n < 1 || n > kMaxGenericRegions) return cudaErrorInvalidValue;
   GenericBatch b{};
-  int w = 0, h = 0;
+  b.n = n;
+  b.first[0] = 0;
   for (int i = 0; i < n; ++i) {
     b.r[i] = a[i];
-    w = w > a[i].w2 ? w : a[i].w2;
-    h = h > a[i].h2 ? h : a[i].h2;
+    b.tiles_x[i] = (a[i].w2 + 31) / 32;
+    b.first[i + 1] = b.first[i] + b.tiles_x[i] * ((a[i].h2 + 7) / 8);
   }
-  const dim3 block(32, 8);
-  const dim3 grid((w + 31) / 32, (h + 7) / 8, n);
-  generic_step_kernel<<<grid, block, 0, st>>>(b);
+  if (b.first[n] == 0) return cudaSuccess;
+  generic_step_kernel<<<b.first[n], dim3(32, 8), 0, st>>>(b);
   return cudaGetLastError();
 }
 
