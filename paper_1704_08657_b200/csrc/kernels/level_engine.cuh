@@ -500,9 +500,10 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
 // two vertically adjacent chunks then reach their shared boundary rows at the
 // same time (both start there, or both end there), so the warm-up rows one of
 // them re-reads are still in L2 instead of coming from HBM again. Only the
-// vector kernels of the per-level launches carry the bottom-up variant (ALT):
-// it is a bandwidth optimisation for large levels, and every extra body of a
-// fully unrolled plan costs minutes of nvcc time.
+// vector image-input kernels (forward levels) of programs with short
+// sub-steps (P::kAlt) carry the bottom-up variant (ALT): a second unrolled
+// body costs registers and nvcc time, and measured slower for the planar and
+// image-output (inverse) kernels.
 template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool ALT>
 __device__ __forceinline__ void level_dispatch(const LevelArgs& a, const int wid) {
   const int c = wid / a.nstrips;
@@ -526,7 +527,7 @@ level_kernel(const LevelArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && P::kAlt>(a, wid);
+  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && IN_IL && P::kAlt>(a, wid);
 }
 
 // ------------------------------------------------ wavefront pyramid kernel
