@@ -108,8 +108,10 @@ typedef struct {
   int32_t forward;
   int32_t extension;
   int32_t fused_multiply_add;
-  int32_t generic;          /* 1: runs on the generic executor (one pass per sub-step:
-                               symmetric extension or no ahead-of-time kernel) */
+  int32_t generic;          /* 1: runs on the generic executor only (one pass per
+                               sub-step: no ahead-of-time kernel for the program);
+                               0: fused kernel (symmetric extension: plus the border
+                               bands on the generic executor) */
 } dwt2d_plan_info;
 
 /* --- plans -------------------------------------------------------------- */
@@ -174,7 +176,8 @@ DWT2D_B200_API int dwt2d_inverse_level_strip(const dwt2d_plan* plan, const float
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by
  * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL
- * bands: at least dwt2d_workspace_bytes() bytes, or NULL to let the library
+ * bands (every level's in its own slot) and the wavefront scheduler's
+ * counters: at least dwt2d_workspace_bytes() bytes, or NULL to let the library
  * take it from the stream-ordered allocator. Width and height must be
  * divisible by 2^levels. */
 DWT2D_B200_API size_t dwt2d_workspace_bytes(int width, int height, int levels);

@@ -38,6 +38,7 @@ struct LevelArgs {
   int vec;              // 1: vector fast path valid (w2 % CW == 0, 16 B aligned)
   int reverse;          // 1: hand out chunks bottom-up (see capi.cpp forward_mallat)
   int alternate;        // 1: odd chunks stream bottom-up (shared warm-up rows hit L2)
+  int staged;           // 1: interleaved input rows staged in shared memory by TMA
   // Row strips (multi-GPU): when halo != 0, component rows above the strip
   // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from
   // halo_bot (row y - h2) instead of wrapping periodically inside the strip.

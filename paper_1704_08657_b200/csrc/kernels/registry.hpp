@@ -36,6 +36,16 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if constexpr (IN_IL) {
+    if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader)
+      auto k = level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>;
+      static const cudaError_t attr_ok =
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<P::kCW>());
+      if (attr_ok != cudaSuccess) return attr_ok;
+      cfg.dynamicSmemBytes = staged_bytes<P::kCW>();
+      return cudaLaunchKernelEx(&cfg, k, a);
+    }
+  }
   if (a.vec) return cudaLaunchKernelEx(&cfg, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true>, a);
   return cudaLaunchKernelEx(&cfg, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, false>, a);
 }
@@ -43,8 +53,8 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
 template <class P, bool IN_IL, bool OUT_IL>
 int level_occupancy() {
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &blocks, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true>, kWarpsPerCta * 32, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true>,
+                                                    kWarpsPerCta * 32, 0) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }

@@ -172,6 +172,22 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
   a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, a.h2) : chunk_rows_for(p, a.h2, a.nstrips);
+  // TMA-staged input rows (level_engine.cuh: TmaRowReader) for forward levels
+  // that stream at least 512 MiB from HBM: level 1 of 16384^2 346 vs 355 us,
+  // with ~10 waves of 32-row chunks (64-row chunks: 364 us). Smaller levels
+  // keep register prefetch: there the stage set-up per work item costs more
+  // than it hides (16384^2 pyramid levels 2..8 +16 us with staging).
+  {
+    const char* env = std::getenv("DWT2D_TMA");
+    const size_t bytes = size_t(a.w2) * size_t(a.h2) * 16;
+    a.staged = layout == kFromImage && !(env && *env == '0') &&
+               (bytes >= (size_t(512) << 20) || (env && *env == '2')) ? 1 : 0;
+    if (a.staged && chunk_override <= 0 && !std::getenv("DWT2D_CHUNK_ROWS")) {
+      const long long resident = resident_warps(p);
+      const long long rows_total = (long long)a.h2 * a.nstrips;
+      a.chunk_rows = int(std::max<long long>(8, std::min<long long>(a.h2, (rows_total + 10 * resident - 1) / (10 * resident))));
+    }
+  }
   a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
   // bottom-up odd chunks pay once the level streams from HBM (their shared
   // warm-up rows then meet in L2: 4096^2 single level 30.7 vs 32.8 us); a
@@ -194,6 +210,7 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
     }
   }
   a.vec = vec ? 1 : 0;
+  if (!a.vec) a.staged = 0;
 }
 
 void keep_pool_memory() {

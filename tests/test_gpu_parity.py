@@ -211,6 +211,39 @@ def test_wavefront_pyramid_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
         assert torch.equal(a, b), (W, H, L, c1, cd)
 
 
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
+                                     ("dd137", "nonseparable-lifting", True),
+                                     ("cdf97", "nonseparable-convolution", False)])
+def test_tma_staged_rows_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+    """Input rows staged by TMA bulk copies (forced on every size with
+    DWT2D_TMA=2) give the same bits as register prefetch: images narrower
+    than one warp strip (several wraps per row), strips crossing the right
+    edge, ragged chunks, pitched input views, pyramids."""
+    import torch
+    plan = dwt.Plan(w, s, optimized=opt)
+    for W, H in [(64, 40), (256, 200), (2400, 96), (1024, 1024)]:
+        base = torch.from_numpy(O.random_image(W + 64, H, 9)).to(cuda)
+        for img in (base[:, :W].contiguous(), base[:, 32:32 + W]):  # dense and pitched
+            for chunk in ["0", "5", "32"]:
+                if chunk == "0":
+                    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
+                else:
+                    monkeypatch.setenv("DWT2D_CHUNK_ROWS", chunk)
+                monkeypatch.setenv("DWT2D_TMA", "0")
+                a = plan.forward_level(img)
+                monkeypatch.setenv("DWT2D_TMA", "2")
+                b = plan.forward_level(img)
+                for j in range(4):
+                    assert torch.equal(a[j], b[j]), (W, H, chunk, j)
+    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
+    img = torch.from_numpy(O.random_image(1024, 768, 5)).to(cuda)
+    monkeypatch.setenv("DWT2D_TMA", "0")
+    a = plan.forward_mallat(img, 5)
+    monkeypatch.setenv("DWT2D_TMA", "2")
+    b = plan.forward_mallat(img, 5)
+    assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("first", [2, 3, 5])
 def test_deep_level_wavefront_bit_exact(dwt, cuda, first, monkeypatch):
     """Levels 1..first-1 one launch each, levels first..L as one wavefront:

@@ -113,14 +113,17 @@ class VirtualRing:
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("tma", ["0", "2"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
                                                 ("cdf97", "separable-convolution", False),
                                                 ("dd137", "nonseparable-lifting", True)])
-def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt):
+def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, tma, monkeypatch):
     """The halo-row path of the fused kernel reproduces the single-GPU
-    pyramid bit for bit (same arithmetic; halo rows are the same data)."""
+    pyramid bit for bit (same arithmetic; halo rows are the same data), with
+    register prefetch (DWT2D_TMA=0) and with TMA-staged rows (=2)."""
     import paper_1704_08657_b200 as dwt
+    monkeypatch.setenv("DWT2D_TMA", tma)
     plan = dwt.Plan(wavelet, scheme, optimized=opt)
     up, down = plan.info["reach_up"], plan.info["reach_down"]
     W, Hs, L = 256, 128, 4
