@@ -367,53 +367,45 @@ template <int CW, bool UPW>
 struct TmaRowReader {
   static constexpr int kRowF4 = 32 * CW / 2;  // float4 per image row of the warp
   static constexpr int kTotal = 32 * 8 * CW;   // bytes per image row of the warp
+  RowReader<CW, true, false, false, UPW> g;    // row walk (periodic wrap / halo segments, no division)
   float4* stage0;
   unsigned long long* bar;
-  int xw0, first;  // first image column of lane 0 (wrapped), bytes up to the right edge
-  int next_row, issued, fetched, rows;
+  int xw0, first;  // first image column of lane 0 (wrapped), bytes up to the right image edge
+  int issued, fetched, rows;
   unsigned phase_bits;
 
   __device__ __forceinline__ void issue_row(const LevelArgs& a) {
     const int lane = threadIdx.x & 31;
-    if (issued < rows && lane < 2) {
-      const int s = issued % kStages;
-      const float* src;  // image row 2n + lane of component row next_row
-      long long pitch;
-      int n = next_row;
-      if (a.halo && n < 0) {
-        src = a.halo_top[0], pitch = a.halo_top_pitch[0], n += a.up;
-      } else if (a.halo && n >= a.h2) {
-        src = a.halo_bot[0], pitch = a.halo_bot_pitch[0], n -= a.h2;
-      } else {
-        src = a.in[0], pitch = a.in_pitch[0];
-        if (!a.halo) n = wrap(n, a.h2);
-      }
-      const float* row = src + (2ll * n + lane) * pitch;
-      const unsigned b = smem_addr(bar + s);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * 32 * 8 * CW)
+    if (issued < rows) {
+      if (lane < 2) {  // lane py copies image row 2n + py of component row n
+        const int s = issued & (kStages - 1);
+        const float* row = g.rowp[0] + (lane ? g.half : 0ll);
+        const unsigned b = smem_addr(bar + s);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * kTotal) : "memory");
+        const unsigned dst = smem_addr(stage0 + s * 2 * kRowF4 + lane * kRowF4);
+        // periodic columns: one copy of `first` bytes from column xw0, the
+        // rest (strips crossing the right image edge, images narrower than a
+        // strip) from column 0 on
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(row + xw0), "r"(first), "r"(b)
                      : "memory");
-      const unsigned dst = smem_addr(stage0 + s * 2 * kRowF4 + lane * kRowF4);
-      // periodic columns: one copy of `first` bytes from column xw0, the rest
-      // (strips crossing the right image edge, images narrower than a strip)
-      // from column 0 on
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                   "l"(row + xw0), "r"(first), "r"(b)
-                   : "memory");
-      if (first < kTotal) {
-        const int W = 2 * a.w2;
-        for (int done = first; done < kTotal;) {
-          const int bytes = min(kTotal - done, W * 4);
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           dst + unsigned(done)),
-                       "l"(row), "r"(bytes), "r"(b)
-                       : "memory");
-          done += bytes;
+        if (first < kTotal) {
+          const int W = 2 * a.w2;
+          for (int done = first; done < kTotal;) {
+            const int bytes = min(kTotal - done, W * 4);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dst + unsigned(done)),
+                "l"(row), "r"(bytes), "r"(b)
+                : "memory");
+            done += bytes;
+          }
         }
       }
+      g.advance(a);
     }
-    if (issued < rows) next_row += UPW ? -1 : 1;
     ++issued;
   }
 
@@ -423,10 +415,10 @@ struct TmaRowReader {
     bar = reinterpret_cast<unsigned long long*>(level_smem) + warp * kStages;
     stage0 = reinterpret_cast<float4*>(level_smem + ((kWarpsPerCta * kStages * 8 + 127) / 128) * 128) +
              warp * kStages * 2 * kRowF4;
+    g.init(a, 0, first_row);
     const int W = 2 * a.w2;
     xw0 = wrap(2 * (xc - lane * CW), W);
     first = min(kTotal, (W - xw0) * 4);
-    next_row = first_row;
     issued = fetched = 0;
     rows = nrows;
     phase_bits = 0;
@@ -440,7 +432,7 @@ struct TmaRowReader {
 
   __device__ __forceinline__ void load(const LevelArgs& a, float (&d)[4][CW]) {
     const int lane = threadIdx.x & 31;
-    const int s = fetched % kStages;
+    const int s = fetched & (kStages - 1);
     const unsigned b = smem_addr(bar + s), par = (phase_bits >> s) & 1u;
     unsigned ok = 0;
     do {
