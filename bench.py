@@ -21,7 +21,8 @@ HBM (no explicit flush). nvidia-smi samples clocks during the timed region.
 Metric and traffic model: pixels of the original image per second, and the
 reference's own traffic model of 8 B per pixel per level (read + write
 float32, proj/src/bench.cpp:84-85), i.e. 10.667 B per original pixel for 8
-levels. roofline: the level-1 kernel (the dominant launch) at 8 B/pixel over
+levels. roofline: the dominant launch — levels 1+2 fused in one pass
+(pair_engine.cuh; 8 B/pixel/level for both levels) or level 1 alone — over
 its measured duration vs the measured copy bandwidth in MEASURED_PEAKS.json.
 """
 from __future__ import annotations
@@ -66,9 +67,10 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram bytes per level-1 launch from the committed ncu capture, if any."""
-    p = ROOT / "profiles" / "ncu_level1_summary.json"
+def ncu_traffic(name="ncu_level1_summary.json"):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture, if any."""
+    p = ROOT / "profiles" / name
     if p.exists():
         try:
             d = json.loads(p.read_text())
@@ -357,8 +359,15 @@ def main():
 
     if rank == 0:
         peak, peak_src = peaks()
-        l1_bytes = 8.0 * W * H
+        # the dominant kernel: level 1, or levels 1+2 fused in one pass
+        # (pair_engine.cuh: one launch fewer per pyramid, the first event
+        # pair then brackets both levels)
+        fused12 = n == 1 and launches_captured == args.steps * (LEVELS - 1)
+        l1_bytes = 8.0 * W * H * (1.25 if fused12 else 1.0)
         achieved = l1_bytes / (level_ms[0] * 1e-3) / 1e9
+        kernel_desc = ("levels 1+2 fused (16384^2 -> LL_2 + 6 detail bands, LL_1 kept on chip), "
+                       "8 B/pixel/level algorithmic" if fused12 else
+                       "level 1 (16384^2 -> 4 x 8192^2), 8 B/pixel algorithmic")
         pyr_bytes = sum(8.0 * (W >> l) * (H >> l) for l in range(LEVELS))
         cpu = None
         if not args.no_cpu_baseline:
@@ -378,9 +387,10 @@ def main():
             "pyramid_hbm_gbs_per_gpu": pyr_bytes / (ms_per_step * 1e-3) / 1e9,
             "levels_ms": [round(x, 5) for x in level_ms],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
-                         "kernel": "level 1 (16384^2 -> 4 x 8192^2), 8 B/pixel algorithmic",
-                         "peak_source": peak_src},
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic("ncu_pair_summary.json" if fused12 else "ncu_level1_summary.json"),
+                         "algorithmic_bytes": l1_bytes,
+                         "kernel": kernel_desc, "peak_source": peak_src},
             "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
                     "h2d_bytes_per_step": int(W * H * 4), "d2h_bytes_per_step": int(W * H * 4),
                     "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if n == 1 else

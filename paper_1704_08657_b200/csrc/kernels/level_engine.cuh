@@ -503,6 +503,19 @@ struct RowWriter {
   // whether this lane's columns are inside the image (fixed per lane)
   __device__ __forceinline__ bool lane_in_range() const { return VEC ? xc + CW <= w2 : xc < w2; }
 
+  // planar vector rows of the three detail bands only (the LL band of a
+  // level that feeds the next level in the same pass is not written)
+  __device__ __forceinline__ void store_details(const float (&v)[4][CW]) {
+    static_assert(VEC && !IL && (CW == 4 || CW == 2), "detail rows: planar vector output");
+    sfor<1, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      if constexpr (CW == 4)
+        st_vec(p[j], make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), true);
+      else
+        st_vec(p[j], make_float2(v[j][0], v[j][1]), true);
+    });
+  }
+
   __device__ __forceinline__ void store(const float (&v)[4][CW]) {
     if constexpr (VEC) {
       if constexpr (IL) {

@@ -53,6 +53,16 @@ struct LevelArgs {
 
 using LevelLaunch = cudaError_t (*)(const LevelArgs&, cudaStream_t);
 
+// Levels 1 and 2 of a forward pyramid in one pass (pair_engine.cuh): l1 is
+// the image level (its LL band is never written: l1.out[0] unused), l2 the
+// next level (l2.in unused). Work items: (strip, chunk of level-2 rows).
+constexpr int kPairLanes = 28;  // lanes 2..29 store both levels
+struct PairArgs {
+  LevelArgs l1, l2;
+  int nstrips, chunk_rows, nchunks;
+};
+using PairLaunch = cudaError_t (*)(const PairArgs&, cudaStream_t);
+
 // Wavefront pyramid (level_engine.cuh: wave_kernel): every level of a
 // forward pyramid in one persistent launch. `state` (device, zeroed before
 // the launch) holds the ticket counter, then per level one completion counter
@@ -83,6 +93,8 @@ struct PlanEntry {
   LevelLaunch from_image;      // interleaved -> 4 planes (forward levels)
   LevelLaunch to_image;        // 4 planes -> interleaved (inverse levels)
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
+  PairLaunch pair;             // levels 1+2 in one pass (forward plans with reach <= 2, CW 4)
+  LevelOccupancy pair_occupancy;
   WaveLaunch wave;             // whole forward pyramid in one launch (forward plans)
   LevelOccupancy wave_occupancy;
 };

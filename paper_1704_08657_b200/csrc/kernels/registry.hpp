@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "level_engine.cuh"
+#include "pair_engine.cuh"
 #include "level_types.hpp"
 
 namespace dwt2d_b200 {
@@ -62,6 +63,39 @@ int level_occupancy() {
 }
 
 template <class P>
+cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
+  const long long warps = (long long)t.nstrips * t.nchunks;
+  if (warps <= 0) return cudaSuccess;
+  auto k = pair_kernel<P>;
+  static const cudaError_t attr_ok =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<4>());
+  if (attr_ok != cudaSuccess) return attr_ok;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta));
+  cfg.blockDim = dim3(kWarpsPerCta * 32);
+  cfg.dynamicSmemBytes = staged_bytes<4>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, t);
+}
+
+template <class P>
+int pair_occupancy() {
+  int blocks = 0;
+  cudaFuncSetAttribute(pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<4>());
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pair_kernel<P>, kWarpsPerCta * 32, staged_bytes<4>()) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return blocks;
+}
+
+template <class P>
 cudaError_t launch_wave(const WaveArgs& t, int blocks, cudaStream_t st) {
   wave_kernel<P, kPrefetchRows, true, false><<<blocks, kWarpsPerCta * 32, 0, st>>>(t);
   return cudaGetLastError();
@@ -92,6 +126,10 @@ PlanEntry make_entry() {
     e.from_image = &launch_level<P, true, false>;
     e.occupancy = &level_occupancy<P, true, false>;
     e.wave = &launch_wave<P>;
+    if constexpr (PairTraits<P>::ok && P::kAlt) {
+      e.pair = &launch_pair<P>;
+      e.pair_occupancy = &pair_occupancy<P>;
+    }
     e.wave_occupancy = &wave_occupancy<P>;
   } else {
     e.to_image = &launch_level<P, false, true>;

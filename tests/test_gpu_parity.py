@@ -244,6 +244,32 @@ def test_tma_staged_rows_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
+                                     ("cdf97", "separable-lifting", True),
+                                     ("cdf97", "nonseparable-polyconvolution", True)])
+def test_level_pair_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+    """Levels 1 + 2 in one pass (LL_1 kept in registers, pair_engine.cuh;
+    forced on every size with DWT2D_PAIR=2) give the same bits as one launch
+    per level: narrow images (strips wrap), short images (chunks wrap
+    periodically), ragged chunks, pitched input, 2..5 levels."""
+    import torch
+    plan = dwt.Plan(w, s, optimized=opt)
+    assert plan.info["columns_per_lane"] == 4
+    for W, H, L in [(1024, 768, 5), (256, 128, 3), (2400, 96, 2), (4096, 64, 2), (64, 64, 2)]:
+        base = torch.from_numpy(O.random_image(W + 32, H, 13)).to(cuda)
+        for img in (base[:, :W].contiguous(), base[:, 16:16 + W]):
+            monkeypatch.setenv("DWT2D_PAIR", "0")
+            a = plan.forward_mallat(img, L)
+            monkeypatch.setenv("DWT2D_PAIR", "2")
+            for chunk in ["1", "3", "32"]:
+                monkeypatch.setenv("DWT2D_PAIR_CHUNK_ROWS", chunk)
+                before = dwt.launch_count()
+                b = plan.forward_mallat(img, L)
+                torch.cuda.synchronize()
+                assert dwt.launch_count() - before == L - 1, (W, H, L)
+                assert torch.equal(a, b), (W, H, L, chunk)
+
+
 @pytest.mark.parametrize("first", [2, 3, 5])
 def test_deep_level_wavefront_bit_exact(dwt, cuda, first, monkeypatch):
     """Levels 1..first-1 one launch each, levels first..L as one wavefront:
