@@ -658,6 +658,46 @@ const unsigned long long* wave_tickets(const dwt2d_plan& p, const std::vector<gp
   return p.wave_cache.back().d;
 }
 
+// Levels l and l + 1 in one pass (pair_engine.cuh): LL_l never goes to HBM.
+// Used for levels 1+2 where level 1 streams from HBM with TMA-staged rows
+// (>= 512 MiB). DWT2D_PAIR=0 disables it, =2 forces it for levels 1+2 on any
+// size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
+// Returns false (nothing launched) when the pair is not eligible.
+bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::LevelArgs& lb, int l, cudaStream_t st) {
+  if (!p.entry || !p.entry->pair || p.extension != DWT2D_PERIODIC) return false;
+  const char* env = std::getenv("DWT2D_PAIR");
+  if (env && *env == '0') return false;
+  const bool force = env && *env == '2';
+  const char* deep = std::getenv("DWT2D_PAIR_DEEP");
+  if (l > 1 && !(deep && *deep == '1')) return false;
+  gpu::PairArgs t{};
+  t.l1 = la, t.l2 = lb;
+  prepare(p, t.l1, kFromImage);
+  prepare(p, t.l2, kFromImage);
+  if (!(t.l1.vec && t.l2.vec && (t.l1.staged || force || l > 1))) return false;
+  // whole waves of ~256-row chunks (measured at 16384^2: one wave of 256-row
+  // chunks 432 us, 1.4 waves of 192 rows 593 us, 32-row chunks 488 us: the
+  // 2(U+L)+U+L warm-up rows per chunk and partial waves both cost at 8 warps
+  // per SM)
+  t.nstrips = (t.l1.w2 + gpu::kPairLanes * 4 - 1) / (gpu::kPairLanes * 4);
+  static thread_local const gpu::PlanEntry* cached = nullptr;
+  static thread_local int per_sm = 0;
+  if (cached != p.entry) {
+    cached = p.entry;
+    per_sm = p.entry->pair_occupancy ? p.entry->pair_occupancy() : 0;
+  }
+  const long long resident = (long long)std::max(1, per_sm) * gpu::kWarpsPerCta * sm_count();
+  const long long per_wave = std::max<long long>(1, resident / t.nstrips);  // chunks per full wave
+  const long long waves = std::max<long long>(1, (t.l2.h2 + 128 * per_wave) / (256 * per_wave));
+  long long chunk = (t.l2.h2 + waves * per_wave - 1) / (waves * per_wave);
+  if (const char* c = std::getenv("DWT2D_PAIR_CHUNK_ROWS")) chunk = std::max(1, std::atoi(c));
+  t.chunk_rows = int(std::min<long long>(chunk, t.l2.h2));
+  t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
+  cuda_check(p.entry->pair(t, st), "level pair kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return true;
+}
+
 void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W, int H, int levels,
                     float* out, size_t out_pitch, float* ws, cudaStream_t st,
                     void* const* events = nullptr) {
@@ -705,44 +745,6 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     wave = t.tickets != nullptr;
   }
   const int last_single = wave ? first - 1 : levels;
-  // levels 1 and 2 in one pass (pair_engine.cuh): LL_1 never goes to HBM.
-  // Used where level 1 streams from HBM with TMA-staged rows (>= 512 MiB);
-  // DWT2D_PAIR=0 disables it, =2 forces it on any size (tests).
-  int first_single = 1;
-  if (!wave && levels >= 2 && p.entry && p.entry->pair && p.extension == DWT2D_PERIODIC) {
-    const char* env = std::getenv("DWT2D_PAIR");
-    const bool force = env && *env == '2';
-    if (!(env && *env == '0')) {
-      gpu::PairArgs t{};
-      t.l1 = lv[0], t.l2 = lv[1];
-      prepare(p, t.l1, kFromImage);
-      prepare(p, t.l2, kFromImage);
-      if (t.l1.vec && t.l2.vec && (t.l1.staged || force)) {
-        // whole waves of ~256-row chunks (measured at 16384^2: one wave of
-        // 256-row chunks 432 us, 1.4 waves of 192 rows 593 us, 32-row chunks
-        // 488 us: the 2(U+L)+U+L warm-up rows per chunk and partial waves
-        // both cost at 8 warps per SM)
-        t.nstrips = (t.l1.w2 + gpu::kPairLanes * 4 - 1) / (gpu::kPairLanes * 4);
-        static thread_local const gpu::PlanEntry* cached = nullptr;
-        static thread_local int per_sm = 0;
-        if (cached != p.entry) {
-          cached = p.entry;
-          per_sm = p.entry->pair_occupancy ? p.entry->pair_occupancy() : 0;
-        }
-        const long long resident = (long long)std::max(1, per_sm) * gpu::kWarpsPerCta * sm_count();
-        const long long per_wave = std::max<long long>(1, resident / t.nstrips);  // chunks per full wave
-        const long long waves = std::max<long long>(1, (t.l2.h2 + 128 * per_wave) / (256 * per_wave));
-        long long chunk = (t.l2.h2 + waves * per_wave - 1) / (waves * per_wave);
-        if (const char* c = std::getenv("DWT2D_PAIR_CHUNK_ROWS")) chunk = std::max(1, std::atoi(c));
-        t.chunk_rows = int(std::min<long long>(chunk, t.l2.h2));
-        t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
-        cuda_check(p.entry->pair(t, st), "level pair kernel launch");
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        if (events) record(events[1], st), record(events[2], st);
-        first_single = 3;
-      }
-    }
-  }
   // tuning: DWT2D_LEVEL_CHUNK_ROWS="r1,r2,..." overrides the chunk rows of
   // the per-level launches (0 or missing entries keep the policy)
   std::vector<int> level_chunks;
@@ -752,7 +754,12 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
       while (*q && *q != ',') ++q;
       if (*q == ',') ++q;
     }
-  for (int l = first_single; l <= last_single; ++l) {
+  for (int l = 1; l <= last_single; ++l) {
+    if (l + 1 <= last_single && launch_pair(p, lv[l - 1], lv[l], l, st)) {
+      if (events) record(events[l], st), record(events[l + 1], st);
+      ++l;
+      continue;
+    }
     gpu::LevelArgs a = lv[l - 1];
     // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
     // level l wrote last, which are still in L2 (LL uses normal stores, the
