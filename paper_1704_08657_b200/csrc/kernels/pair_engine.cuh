@@ -29,6 +29,27 @@
 namespace dwt2d_b200 {
 namespace gpu {
 
+// Planar vector rows addressed from the launch parameters on every store
+// (row index and lane column only: no per-band pointers or pitches held in
+// registers — the fused pair is register-bound).
+template <int CW>
+struct LeanRowWriter {
+  int xc, y;
+  __device__ __forceinline__ void init(int xc_, int first_row) { xc = xc_, y = first_row; }
+  __device__ __forceinline__ void advance() { ++y; }
+  template <int J0>
+  __device__ __forceinline__ void store_from(const LevelArgs& a, const float (&v)[4][CW]) {
+    sfor<J0, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      float* q = a.out[j] + (long long)y * a.out_pitch[j] + xc;
+      if constexpr (CW == 4)
+        st_vec(q, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
+      else
+        st_vec(q, make_float2(v[j][0], v[j][1]), j != 0);
+    });
+  }
+};
+
 template <class P>
 struct PairTraits {
   using M = Meta<P>;
@@ -73,12 +94,12 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
 
   TmaRowReader<CW1, false> rd;
   rd.init(a1, xc1, n01, rows1);
-  RowWriter<CW1, false, true, false> w1;
-  w1.init(a1, xc1, yfirst1);
-  RowWriter<CW2, false, true, false> w2;
-  w2.init(a2, xc2, yfirst2);
-  const bool st1 = core && w1.lane_in_range();
-  const bool st2 = core && w2.lane_in_range();
+  LeanRowWriter<CW1> w1;
+  w1.init(xc1, yfirst1);
+  LeanRowWriter<CW2> w2;
+  w2.init(xc2, yfirst2);
+  const bool st1 = core && xc1 + CW1 <= a1.w2;
+  const bool st2 = core && xc2 + CW2 <= a2.w2;
   rd.load(a1, ring1[0][SC::slot(0, 0, 0)]);
 
   for (int it = 0; it < iters; it += UNR) {
@@ -106,7 +127,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
       sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW1, false>(ring1); });
       constexpr int so = SC::slot(S, u, 0);
       const int y1 = yfirst1 + i;
-      if (y1 >= 2 * m0 && y1 < 2 * m1 && st1) w1.store_details(ring1[S][so]);
+      if (y1 >= 2 * m0 && y1 < 2 * m1 && st1) w1.store_from<1>(a1, ring1[S][so]);
       w1.advance();
       // ------------------------------------------- LL_1 row -> level 2
       const int k = i - (U + L);  // LL_1 row 2 * n02 + k
@@ -146,7 +167,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
           });
           sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u2, D, CW2, false>(ring2); });
           const int y2 = yfirst2 + i2;
-          if (y2 >= m0 && y2 < m1 && st2) w2.store(ring2[S][SC::slot(S, u2, 0)]);
+          if (y2 >= m0 && y2 < m1 && st2) w2.store_from<0>(a2, ring2[S][SC::slot(S, u2, 0)]);
           w2.advance();
         }
       }
