@@ -558,6 +558,28 @@ struct RowWriter {
   }
 };
 
+// Planar vector rows addressed from the launch parameters on every store
+// (row index and lane column only: no per-band pointers or pitches held in
+// registers: fewer live registers in the register-bound fused level pair;
+// in the single-level kernels it measured neutral to slower).
+template <int CW, bool UPW = false>
+struct LeanRowWriter {
+  int xc, y;
+  __device__ __forceinline__ void init(int xc_, int first_row) { xc = xc_, y = first_row; }
+  __device__ __forceinline__ void advance() { y += UPW ? -1 : 1; }
+  template <int J0>
+  __device__ __forceinline__ void store_from(const LevelArgs& a, const float (&v)[4][CW]) {
+    sfor<J0, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      float* q = a.out[j] + (long long)y * a.out_pitch[j] + xc;
+      if constexpr (CW == 4)
+        st_vec(q, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
+      else
+        st_vec(q, make_float2(v[j][0], v[j][1]), j != 0);
+    });
+  }
+};
+
 // ------------------------------------------------------------- kernel
 
 // One work item: warp `wid` streams its (strip, chunk) of the level, top-down

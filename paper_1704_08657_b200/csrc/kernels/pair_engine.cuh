@@ -29,27 +29,6 @@
 namespace dwt2d_b200 {
 namespace gpu {
 
-// Planar vector rows addressed from the launch parameters on every store
-// (row index and lane column only: no per-band pointers or pitches held in
-// registers — the fused pair is register-bound).
-template <int CW>
-struct LeanRowWriter {
-  int xc, y;
-  __device__ __forceinline__ void init(int xc_, int first_row) { xc = xc_, y = first_row; }
-  __device__ __forceinline__ void advance() { ++y; }
-  template <int J0>
-  __device__ __forceinline__ void store_from(const LevelArgs& a, const float (&v)[4][CW]) {
-    sfor<J0, 4>([&](auto J_) {
-      constexpr int j = decltype(J_)::value;
-      float* q = a.out[j] + (long long)y * a.out_pitch[j] + xc;
-      if constexpr (CW == 4)
-        st_vec(q, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
-      else
-        st_vec(q, make_float2(v[j][0], v[j][1]), j != 0);
-    });
-  }
-};
-
 template <class P>
 struct PairTraits {
   using M = Meta<P>;
