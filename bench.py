@@ -251,9 +251,10 @@ def run_single(args, plan, img, out, dev):
 
 
 def run_sharded(args, plan, img, out, dev, n):
-    """N > 1: each rank owns a 16384-row strip; every level exchanges 4+4
-    halo rows with its ring neighbours (NCCL) and runs the fused strip
-    kernel. Eager launches (NCCL P2P per level), events around each level."""
+    """N > 1: each rank owns a 16384-row strip; levels 1+2 exchange 12+12
+    halo rows with the ring neighbours (NCCL) and run as one fused pass on the
+    strip, every later level exchanges 4+4 rows and runs the fused strip
+    kernel. Eager launches (NCCL P2P per level), events around each kernel."""
     import torch
     import torch.distributed as dist
     import paper_1704_08657_b200 as dwt
@@ -269,8 +270,19 @@ def run_sharded(args, plan, img, out, dev, n):
         cur_events.append((e0, e1))
         return r
 
+    pair = plan.has_pair and os.environ.get("DWT2D_PAIR", "1") != "0"
+
+    def pair_fn(cur, top, bottom):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = plan.forward_pair_strip(cur, top, bottom)
+        e1.record()
+        cur_events.append((e0, e1))
+        return r
+
+    pf = pair_fn if pair else None
     for _ in range(args.warmup):
-        S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out)
+        S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out, pair_fn=pf)
     torch.cuda.synchronize()
     cur_events.clear()
     launches0 = dwt.launch_count()
@@ -280,7 +292,7 @@ def run_sharded(args, plan, img, out, dev, n):
     with ClockSampler(dev.index or 0) as clk:
         t0.record()
         for _ in range(args.steps):
-            S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out)
+            S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out, pair_fn=pf)
         t1.record()
         t1.synchronize()
         dist.barrier()
@@ -289,8 +301,10 @@ def run_sharded(args, plan, img, out, dev, n):
     total = torch.tensor([t0.elapsed_time(t1)], device=dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
-    level_ms = [statistics.mean(cur_events[k * LEVELS + l][0].elapsed_time(cur_events[k * LEVELS + l][1])
-                                for k in range(args.steps)) for l in range(LEVELS)]
+    per = LEVELS - 1 if pair else LEVELS  # kernels per pyramid
+    kern_ms = [statistics.mean(cur_events[k * per + l][0].elapsed_time(cur_events[k * per + l][1])
+                               for k in range(args.steps)) for l in range(per)]
+    level_ms = [kern_ms[0], 0.0] + kern_ms[1:] if pair else kern_ms
     return SIZE * SIZE * n / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
 
 
@@ -347,7 +361,8 @@ def main():
 
         def e2e_step():
             dev_in.copy_(host_img, non_blocking=True)
-            S.forward_mallat_strips(S.gpu_level_fn(plan), dev_in, LEVELS, UP, DOWN, ex, out=dev_out)
+            S.forward_mallat_strips(S.gpu_level_fn(plan), dev_in, LEVELS, UP, DOWN, ex, out=dev_out,
+                                    pair_fn=S.gpu_pair_fn(plan))
             host_out.copy_(dev_out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     e2e_step()
@@ -370,7 +385,7 @@ def main():
         # the dominant kernel: level 1, or levels 1+2 fused in one pass
         # (pair_engine.cuh: one launch fewer per pyramid, the first event
         # pair then brackets both levels)
-        fused12 = n == 1 and launches_captured == args.steps * (LEVELS - 1)
+        fused12 = launches_captured == args.steps * (LEVELS - 1)
         l1_bytes = 8.0 * W * H * (1.25 if fused12 else 1.0)
         achieved = l1_bytes / (level_ms[0] * 1e-3) / 1e9
         kernel_desc = ("levels 1+2 fused (16384^2 -> LL_2 + 6 detail bands, LL_1 kept on chip), "
@@ -405,8 +420,8 @@ def main():
                             "pinned host strip -> H2D -> strips.forward_mallat_strips (C ABI strip "
                             "kernel + NCCL halos) -> D2H, per rank")},
             "gpu_launches": int(launches_captured),
-            "halo_exchange": ("NCCL batched send/recv of 4+4 image rows per level per rank (ring)"
-                              if n > 1 else None),
+            "halo_exchange": ("NCCL batched send/recv per rank (ring): 12+12 image rows for the fused "
+                              "levels 1+2, 4+4 rows for each later level" if n > 1 else None),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }

@@ -164,6 +164,21 @@ DWT2D_B200_API int dwt2d_forward_level_strip(const dwt2d_plan* plan, const float
                                              const float* bottom, size_t halo_pitch,
                                              float* const out[4], const size_t out_pitch[4],
                                              void* stream);
+/* Levels 1 and 2 of a strip in one pass (the fused level pair; LL_1 never
+ * goes to memory): `top`/`bottom` hold the 6*reach_up / 6*reach_down image
+ * rows directly above/below the strip (12 and 12 for CDF 9/7). Outputs: the
+ * strip's rows of level 1's HL, LH, HH (out1, each width/2 x height/2) and of
+ * level 2's LL, HL, LH, HH (out2, each width/4 x height/4). Sides must be
+ * multiples of 4 (16 for the vector path, required), rows 16-byte aligned.
+ * DWT2D_EUNSUPPORTED when dwt2d_plan_has_pair(plan) is 0 (programs reaching
+ * more than 2 component columns, symmetric extension). */
+DWT2D_B200_API int dwt2d_plan_has_pair(const dwt2d_plan* plan);
+DWT2D_B200_API int dwt2d_forward_pair_strip(const dwt2d_plan* plan, const float* image, size_t pitch,
+                                            int width, int height, const float* top,
+                                            const float* bottom, size_t halo_pitch,
+                                            float* const out1[3], const size_t out1_pitch[3],
+                                            float* const out2[4], const size_t out2_pitch[4],
+                                            void* stream);
 /* Inverse counterpart: four planar band strips (w2 x h2) plus reach_up rows
  * above and reach_down rows below of each band (top[j], bottom[j]) into the
  * strip's 2*h2 image rows. */

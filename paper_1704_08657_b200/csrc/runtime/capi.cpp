@@ -663,18 +663,8 @@ const unsigned long long* wave_tickets(const dwt2d_plan& p, const std::vector<gp
 // (>= 512 MiB). DWT2D_PAIR=0 disables it, =2 forces it for levels 1+2 on any
 // size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
 // Returns false (nothing launched) when the pair is not eligible.
-bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::LevelArgs& lb, int l, cudaStream_t st) {
-  if (!p.entry || !p.entry->pair || p.extension != DWT2D_PERIODIC) return false;
-  const char* env = std::getenv("DWT2D_PAIR");
-  if (env && *env == '0') return false;
-  const bool force = env && *env == '2';
-  const char* deep = std::getenv("DWT2D_PAIR_DEEP");
-  if (l > 1 && !(deep && *deep == '1')) return false;
-  gpu::PairArgs t{};
-  t.l1 = la, t.l2 = lb;
-  prepare(p, t.l1, kFromImage);
-  prepare(p, t.l2, kFromImage);
-  if (!(t.l1.vec && t.l2.vec && (t.l1.staged || force || l > 1))) return false;
+// Chunking and launch of a prepared level pair.
+void run_pair(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
   // whole waves of ~256-row chunks (measured at 16384^2: one wave of 256-row
   // chunks 432 us, 1.4 waves of 192 rows 593 us, 32-row chunks 488 us: the
   // 2(U+L)+U+L warm-up rows per chunk and partial waves both cost at 8 warps
@@ -695,6 +685,30 @@ bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::Level
   t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
   cuda_check(p.entry->pair(t, st), "level pair kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+bool pair_capable(const dwt2d_plan& p) {
+  return p.entry && p.entry->pair && p.extension == DWT2D_PERIODIC;
+}
+
+// Levels l and l + 1 in one pass (pair_engine.cuh): LL_l never goes to HBM.
+// Used for levels 1+2 where level 1 streams from HBM with TMA-staged rows
+// (>= 512 MiB). DWT2D_PAIR=0 disables it, =2 forces it for levels 1+2 on any
+// size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
+// Returns false (nothing launched) when the pair is not eligible.
+bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::LevelArgs& lb, int l, cudaStream_t st) {
+  if (!pair_capable(p)) return false;
+  const char* env = std::getenv("DWT2D_PAIR");
+  if (env && *env == '0') return false;
+  const bool force = env && *env == '2';
+  const char* deep = std::getenv("DWT2D_PAIR_DEEP");
+  if (l > 1 && !(deep && *deep == '1')) return false;
+  gpu::PairArgs t{};
+  t.l1 = la, t.l2 = lb;
+  prepare(p, t.l1, kFromImage);
+  prepare(p, t.l2, kFromImage);
+  if (!(t.l1.vec && t.l2.vec && (t.l1.staged || force || l > 1))) return false;
+  run_pair(p, t, st);
   return true;
 }
 
@@ -1172,6 +1186,40 @@ int dwt2d_forward_level_strip(const dwt2d_plan* p, const float* image, size_t pi
     a.halo = 1, a.up = p->up, a.down = p->down;
     a.w2 = width / 2, a.h2 = height / 2;
     launch(*p, a, kFromImage, as_stream(stream));
+  });
+}
+
+int dwt2d_plan_has_pair(const dwt2d_plan* p) { return p && pair_capable(*p) ? 1 : 0; }
+
+int dwt2d_forward_pair_strip(const dwt2d_plan* p, const float* image, size_t pitch, int width, int height,
+                             const float* top, const float* bottom, size_t halo_pitch, float* const out1[3],
+                             const size_t out1_pitch[3], float* const out2[4], const size_t out2_pitch[4],
+                             void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out1 || !out1_pitch || !out2 || !out2_pitch || !top || !bottom)
+      fail(DWT2D_EINVAL, "null argument");
+    if (width <= 0 || height <= 0 || width % 4 || height % 4)
+      fail(DWT2D_EINVAL, "forward_pair_strip: strip sides must be positive multiples of 4");
+    if (!pair_capable(*p)) fail(DWT2D_EUNSUPPORTED, "forward_pair_strip: no fused level-pair kernel for this plan");
+    gpu::PairArgs t{};
+    gpu::LevelArgs& a = t.l1;
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = image, a.in_pitch[j] = (long long)pitch;
+      a.halo_top[j] = top, a.halo_bot[j] = bottom;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)halo_pitch;
+      a.out[j] = out1[j == 0 ? 0 : j - 1], a.out_pitch[j] = (long long)out1_pitch[j == 0 ? 0 : j - 1];
+      t.l2.out[j] = out2[j], t.l2.out_pitch[j] = (long long)out2_pitch[j];
+      t.l2.in[j] = image, t.l2.in_pitch[j] = (long long)pitch;  // unused by the pair
+    }
+    a.halo = 1, a.up = 3 * p->up, a.down = 3 * p->down;
+    a.w2 = width / 2, a.h2 = height / 2;
+    t.l2.w2 = width / 4, t.l2.h2 = height / 4;
+    prepare(*p, t.l1, kFromImage);
+    prepare(*p, t.l2, kFromImage);
+    if (!t.l1.vec || !t.l2.vec)
+      fail(DWT2D_EINVAL, "forward_pair_strip: needs 16-byte aligned rows and widths divisible by 16");
+    run_pair(*p, t, as_stream(stream));
   });
 }
 

@@ -74,16 +74,34 @@ LevelFn = Callable[[object, object, object], Sequence[object]]
 
 
 def forward_mallat_strips(level_fn: LevelFn, strip, levels: int, up: int, down: int,
-                          exchange: Callable, out=None):
+                          exchange: Callable, out=None, pair_fn: Callable | None = None):
     """Strip-sharded forward pyramid. level_fn(strip, top, bottom) returns
-    the strip's four bands (LL, HL, LH, HH). Works on torch tensors (CPU or
-    CUDA). Returns the rank's strip-Mallat buffer."""
+    the strip's four bands (LL, HL, LH, HH). pair_fn(strip, top, bottom), if
+    given, runs levels 1 and 2 in one pass from 6*up / 6*down halo rows and
+    returns ([HL1, LH1, HH1], [LL2, HL2, LH2, HH2]). Works on torch tensors
+    (CPU or CUDA). Returns the rank's strip-Mallat buffer."""
     import torch
     h0, w0 = strip.shape
     if out is None:
         out = torch.empty_like(strip)
     cur = strip
-    for lvl in range(levels):
+    first = 0
+    if pair_fn is not None and levels >= 2:
+        h, w = cur.shape
+        check_strip(h, w, 3 * up, 3 * down)
+        top, bottom = exchange(cur, 6 * up, 6 * down)
+        (hl1, lh1, hh1), (ll2, hl2, lh2, hh2) = pair_fn(cur, top, bottom)
+        h2, w2, h4, w4 = h // 2, w // 2, h // 4, w // 4
+        out[:h2, w2:w] = hl1
+        out[h2:h, :w2] = lh1
+        out[h2:h, w2:w] = hh1
+        out[:h4, w4:w2] = hl2
+        out[h4:h2, :w4] = lh2
+        out[h4:h2, w4:w2] = hh2
+        if levels == 2:
+            out[:h4, :w4] = ll2
+        cur, first = ll2, 2
+    for lvl in range(first, levels):
         h, w = cur.shape
         check_strip(h, w, up, down)
         top, bottom = exchange(cur, 2 * up, 2 * down)
@@ -125,4 +143,14 @@ def gpu_level_fn(plan, stream=None) -> LevelFn:
     """The product's level function: the fused sm_100a kernel with halo rows."""
     def fn(cur, top, bottom):
         return plan.forward_level_strip(cur, top, bottom, stream=stream)
+    return fn
+
+
+def gpu_pair_fn(plan, stream=None):
+    """The product's fused level pair on a strip (None if the plan has none)."""
+    if not plan.has_pair:
+        return None
+
+    def fn(cur, top, bottom):
+        return plan.forward_pair_strip(cur, top, bottom, stream=stream)
     return fn

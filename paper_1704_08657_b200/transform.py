@@ -151,6 +151,31 @@ class Plan:
                                                 N._P4(*optr), N._S4(*opit), _stream_handle(stream)))
         return list(out)
 
+    @property
+    def has_pair(self) -> bool:
+        """Whether levels 1 and 2 can run fused (forward_pair_strip)."""
+        return bool(N.lib.dwt2d_plan_has_pair(self._h))
+
+    def forward_pair_strip(self, strip, top, bottom, stream=None):
+        """Levels 1 and 2 of a row strip in one pass; `top`/`bottom` are the
+        6*reach_up / 6*reach_down image rows above/below it. Returns
+        (level-1 [HL, LH, HH], level-2 [LL, HL, LH, HH])."""
+        import torch
+        H, W = strip.shape
+        d = strip.device
+        out1 = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=d) for _ in range(3)]
+        out2 = [torch.empty((H // 4, W // 4), dtype=torch.float32, device=d) for _ in range(4)]
+        ptr, pitch = _dev(strip, "strip")
+        tptr, tpitch = _dev(top, "top")
+        bptr, bpitch = _dev(bottom, "bottom")
+        if tpitch != bpitch:
+            raise ValueError("top and bottom halos must share a pitch")
+        p1, s1 = zip(*[_dev(o, "out") for o in out1])
+        p2, s2 = zip(*[_dev(o, "out") for o in out2])
+        N.check(N.lib.dwt2d_forward_pair_strip(self._h, ptr, pitch, W, H, tptr, bptr, tpitch, N._P3(*p1),
+                                               N._S3(*s1), N._P4(*p2), N._S4(*s2), _stream_handle(stream)))
+        return out1, out2
+
     def inverse_level_strip(self, planes: Sequence, tops: Sequence, bottoms: Sequence, image=None,
                             stream=None):
         import torch

@@ -113,15 +113,16 @@ class VirtualRing:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tma", ["0", "2"])
+@pytest.mark.parametrize("tma,pair", [("0", False), ("2", False), ("1", True)])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
                                                 ("cdf97", "separable-convolution", False),
                                                 ("dd137", "nonseparable-lifting", True)])
-def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, tma, monkeypatch):
+def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, tma, pair, monkeypatch):
     """The halo-row path of the fused kernel reproduces the single-GPU
     pyramid bit for bit (same arithmetic; halo rows are the same data), with
-    register prefetch (DWT2D_TMA=0) and with TMA-staged rows (=2)."""
+    register prefetch (DWT2D_TMA=0), TMA-staged rows (=2), and with levels
+    1+2 as one fused pass from 6*up/6*down halo rows (pair)."""
     import paper_1704_08657_b200 as dwt
     monkeypatch.setenv("DWT2D_TMA", tma)
     plan = dwt.Plan(wavelet, scheme, optimized=opt)
@@ -138,7 +139,8 @@ def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme
             torch.cuda.set_device(cuda)
             strip = img[rank * Hs:(rank + 1) * Hs].contiguous()
             outs[rank] = S.forward_mallat_strips(S.gpu_level_fn(plan), strip, L, up, down,
-                                                 ring.exchange_for(rank))
+                                                 ring.exchange_for(rank),
+                                                 pair_fn=S.gpu_pair_fn(plan) if pair else None)
             torch.cuda.synchronize()
         except Exception as e:  # surfaced below
             errors.append(e)
