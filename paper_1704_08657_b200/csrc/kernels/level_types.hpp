@@ -87,6 +87,7 @@ struct PlanEntry {
   const char* key;
   unsigned long long fingerprint;
   int cw;                      // component columns per lane
+  int stage_ok;                // TMA-staged rows measured faster (CW 4 programs)
   int up, down, left, right;   // level reach on the component grid
   long taps_per_quad;
   LevelLaunch planar;          // 4 planes -> 4 planes   (run() API)

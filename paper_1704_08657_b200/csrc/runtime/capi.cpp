@@ -173,15 +173,20 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
   a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, a.h2) : chunk_rows_for(p, a.h2, a.nstrips);
   // TMA-staged input rows (level_engine.cuh: TmaRowReader) for forward levels
-  // that stream at least 512 MiB from HBM: level 1 of 16384^2 346 vs 355 us,
-  // with ~10 waves of 32-row chunks (64-row chunks: 364 us). Smaller levels
-  // keep register prefetch: there the stage set-up per work item costs more
-  // than it hides (16384^2 pyramid levels 2..8 +16 us with staging).
+  // of CW-4 programs (PlanEntry::stage_ok) that stream at least 512 MiB from
+  // HBM: level 1 of 16384^2 346 vs 355 us, with ~10 waves of 32-row chunks
+  // (64-row chunks: 364 us); non-separable polyconvolution opt. 404 vs 524
+  // us, non-separable lifting baseline 411 vs 504 us. CW-2 programs (deep
+  // convolution windows) were slower staged (separable convolution 722 vs
+  // 470 us). Smaller levels keep register prefetch: there the stage set-up
+  // per work item costs more than it hides (16384^2 pyramid levels 2..8 +16
+  // us with staging, 4096^2 single levels +4..+80 us).
   {
     const char* env = std::getenv("DWT2D_TMA");
     const size_t bytes = size_t(a.w2) * size_t(a.h2) * 16;
+    const bool force = env && *env == '2';
     a.staged = layout == kFromImage && !(env && *env == '0') &&
-               (bytes >= (size_t(512) << 20) || (env && *env == '2')) ? 1 : 0;
+               ((bytes >= (size_t(512) << 20) && e.stage_ok) || force) ? 1 : 0;
     if (a.staged && chunk_override <= 0 && !std::getenv("DWT2D_CHUNK_ROWS")) {
       const long long resident = resident_warps(p);
       const long long rows_total = (long long)a.h2 * a.nstrips;
