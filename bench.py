@@ -251,40 +251,28 @@ def run_single(args, plan, img, out, dev):
 
 
 def run_sharded(args, plan, img, out, dev, n):
-    """N > 1: each rank owns a 16384-row strip; levels 1+2 exchange 12+12
-    halo rows with the ring neighbours (NCCL) and run as one fused pass on the
-    strip, every later level exchanges 4+4 rows and runs the fused strip
-    kernel. Eager launches (NCCL P2P per level), events around each kernel."""
+    """N > 1: each rank owns a 16384-row strip. The library's strip driver
+    (dwt2d_forward_mallat_strip, C++) runs the pyramid: levels 1+2 as one
+    fused pass from 12+12 halo rows, every later level from 4+4 rows, the
+    rows coming from the ring neighbours through the exchange callback
+    (NCCL batched send/recv). The timed region is K such pyramids; an
+    untimed pass of the Python per-kernel path with events gives the
+    per-kernel breakdown."""
     import torch
     import torch.distributed as dist
     import paper_1704_08657_b200 as dwt
     from paper_1704_08657_b200 import strips as S
     ex = S.HaloExchange()
-    cur_events = []
+    H, W = img.shape
+    scratch = torch.empty(dwt.native.lib.dwt2d_strip_workspace_bytes(plan._h, W, H, LEVELS) // 4 + 64,
+                          dtype=torch.float32, device=dev)
 
-    def level_fn(cur, top, bottom):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r = plan.forward_level_strip(cur, top, bottom)
-        e1.record()
-        cur_events.append((e0, e1))
-        return r
+    def step():
+        S.gpu_forward_mallat(plan, img, LEVELS, exchange=ex, out=out, scratch=scratch)
 
-    pair = plan.has_pair and os.environ.get("DWT2D_PAIR", "1") != "0"
-
-    def pair_fn(cur, top, bottom):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        r = plan.forward_pair_strip(cur, top, bottom)
-        e1.record()
-        cur_events.append((e0, e1))
-        return r
-
-    pf = pair_fn if pair else None
     for _ in range(args.warmup):
-        S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out, pair_fn=pf)
+        step()
     torch.cuda.synchronize()
-    cur_events.clear()
     launches0 = dwt.launch_count()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
@@ -292,7 +280,7 @@ def run_sharded(args, plan, img, out, dev, n):
     with ClockSampler(dev.index or 0) as clk:
         t0.record()
         for _ in range(args.steps):
-            S.forward_mallat_strips(level_fn, img, LEVELS, UP, DOWN, ex, out=out, pair_fn=pf)
+            step()
         t1.record()
         t1.synchronize()
         dist.barrier()
@@ -301,10 +289,33 @@ def run_sharded(args, plan, img, out, dev, n):
     total = torch.tensor([t0.elapsed_time(t1)], device=dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
+
+    # breakdown (untimed): the same kernels through the Python strip path
+    cur_events = []
+
+    def timed(fn):
+        def w(cur, top, bottom, out=None):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = fn(cur, top, bottom, out=out)
+            e1.record()
+            cur_events.append((e0, e1))
+            return r
+        return w
+
+    pf = S.gpu_pair_fn(plan)
+    pair = pf is not None and os.environ.get("DWT2D_PAIR", "1") != "0"
+    nb = min(args.steps, 20)
+    scratch_out = torch.empty_like(out)
+    for _ in range(nb):
+        S.forward_mallat_strips(timed(S.gpu_level_fn(plan)), img, LEVELS, UP, DOWN, ex, out=scratch_out,
+                                pair_fn=timed(pf) if pair else None)
+    torch.cuda.synchronize()
     per = LEVELS - 1 if pair else LEVELS  # kernels per pyramid
     kern_ms = [statistics.mean(cur_events[k * per + l][0].elapsed_time(cur_events[k * per + l][1])
-                               for k in range(args.steps)) for l in range(per)]
+                               for k in range(nb)) for l in range(per)]
     level_ms = [kern_ms[0], 0.0] + kern_ms[1:] if pair else kern_ms
+    assert torch.equal(scratch_out, out), "strip driver and Python strip path disagree"
     return SIZE * SIZE * n / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
 
 
@@ -318,6 +329,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
                     help="timed region: one CUDA graph of K pyramids, or K eager library calls")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the N>1 strip path (halo exchange + strip kernels) even at N=1 (testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -331,7 +344,13 @@ def main():
     n, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if n > 1:
+    sharded = n > 1 or args.sharded
+    if sharded:
+        if n == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     plan = dwt.Plan(WAVELET, SCHEME, optimized=OPTIMIZED)
@@ -339,7 +358,7 @@ def main():
     # this rank's strip: rows [rank*H, (rank+1)*H) of the W x (n*H) image
     img = random_image(W, H * n, 1, row0=rank * H, rows=H, device=dev)
     out = torch.empty_like(img)
-    if n > 1:
+    if sharded:
         value, ms_per_step, level_ms, launches_captured, clk = run_sharded(args, plan, img, out, dev, n)
     else:
         value, ms_per_step, level_ms, launches_captured, clk = run_single(args, plan, img, out, dev)
@@ -349,7 +368,7 @@ def main():
     # H2D -> 8 levels -> D2H of the whole pyramid, synchronous per step
     host_img = img.cpu().pin_memory()
     host_out = torch.empty_like(host_img).pin_memory()
-    if n == 1:
+    if not sharded:
         hi, ho = host_img.numpy(), host_out.numpy()
 
         def e2e_step():
@@ -361,12 +380,11 @@ def main():
 
         def e2e_step():
             dev_in.copy_(host_img, non_blocking=True)
-            S.forward_mallat_strips(S.gpu_level_fn(plan), dev_in, LEVELS, UP, DOWN, ex, out=dev_out,
-                                    pair_fn=S.gpu_pair_fn(plan))
+            S.gpu_forward_mallat(plan, dev_in, LEVELS, exchange=ex, out=dev_out)
             host_out.copy_(dev_out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     e2e_step()
-    if n > 1:
+    if sharded:
         dist.barrier()
     e2e_t = []
     for _ in range(args.e2e_steps):
@@ -374,7 +392,7 @@ def main():
         e2e_step()
         e2e_t.append(time.perf_counter() - a)
     e2e_s = statistics.median(e2e_t)
-    if n > 1:
+    if sharded:
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
@@ -416,17 +434,17 @@ def main():
                          "kernel": kernel_desc, "peak_source": peak_src},
             "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
                     "h2d_bytes_per_step": int(W * H * 4), "d2h_bytes_per_step": int(W * H * 4),
-                    "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if n == 1 else
-                            "pinned host strip -> H2D -> strips.forward_mallat_strips (C ABI strip "
-                            "kernel + NCCL halos) -> D2H, per rank")},
+                    "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if not sharded else
+                            "pinned host strip -> H2D -> dwt2d_forward_mallat_strip (C ABI strip "
+                            "pyramid driver, NCCL halo callback) -> D2H, per rank")},
             "gpu_launches": int(launches_captured),
             "halo_exchange": ("NCCL batched send/recv per rank (ring): 12+12 image rows for the fused "
-                              "levels 1+2, 4+4 rows for each later level" if n > 1 else None),
+                              "levels 1+2, 4+4 rows for each later level" if sharded else None),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if n > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 

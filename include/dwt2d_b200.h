@@ -188,6 +188,26 @@ DWT2D_B200_API int dwt2d_inverse_level_strip(const dwt2d_plan* plan, const float
                                              const size_t halo_pitch[4], float* image, size_t pitch,
                                              int width, int height, void* stream);
 
+/* Whole forward pyramid of one rank's row strip (width x height, periodic
+ * image of several strips stacked in a ring). Before every level (or the
+ * fused level pair) the library calls `exchange` to fill `top` / `bottom`
+ * (device, `halo_pitch` floats per row) with the `top_rows` / `bottom_rows`
+ * image rows directly above / below the current level input `cur` in the
+ * global image, ordered on `stream` (it may also synchronise); non-zero
+ * aborts with DWT2D_EINVAL. exchange == NULL: the strip is the whole image
+ * (periodic wrap inside it). Output: the strip-Mallat buffer (the strip's
+ * rows of every band in the Mallat layout of the strip). `scratch`: at least
+ * dwt2d_strip_workspace_bytes() bytes, or NULL. */
+typedef int (*dwt2d_halo_fn)(void* user, const float* cur, size_t pitch, int width, int height,
+                             float* top, float* bottom, size_t halo_pitch, int top_rows,
+                             int bottom_rows, void* stream);
+DWT2D_B200_API size_t dwt2d_strip_workspace_bytes(const dwt2d_plan* plan, int width, int height,
+                                                  int levels);
+DWT2D_B200_API int dwt2d_forward_mallat_strip(const dwt2d_plan* plan, const float* strip, size_t pitch,
+                                              int width, int height, int levels, float* out,
+                                              size_t out_pitch, void* scratch, dwt2d_halo_fn exchange,
+                                              void* user, void* stream);
+
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by
  * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL

@@ -836,6 +836,89 @@ void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W
   }
 }
 
+// ---------------------------------------------- strip pyramid (multi-GPU)
+//
+// The whole forward pyramid of one rank's row strip in C++: per level the
+// caller's exchange callback fills the halo rows (NCCL, peer copies, or
+// nothing but a periodic wrap when exchange == NULL), then one fused kernel
+// writes the strip's bands straight into the strip-Mallat buffer; levels 1+2
+// run as one fused pass from 3*up / 3*down component rows of halo.
+
+size_t strip_halo_rows(const dwt2d_plan& p) { return size_t(6) * size_t(std::max(p.up, p.down)); }
+size_t strip_pitch(int W) { return ws_align(size_t(W)); }
+
+size_t strip_workspace_floats(const dwt2d_plan& p, int W, int H, int levels) {
+  return ll_offset(W, H, levels + 1) + 2 * strip_halo_rows(p) * strip_pitch(W);
+}
+
+void strip_exchange(dwt2d_halo_fn ex, void* user, const float* cur, size_t pitch, int w, int h, float* top,
+                    float* bottom, size_t hp, int trows, int brows, cudaStream_t st) {
+  if (ex) {
+    const int rc = ex(user, cur, pitch, w, h, top, bottom, hp, trows, brows, st);
+    if (rc != 0) fail(DWT2D_EINVAL, "strip pyramid: halo exchange callback failed");
+    return;
+  }
+  if (trows > h || brows > h) fail(DWT2D_EINVAL, "strip pyramid: strip thinner than its halo");
+  // a single strip is the whole periodic image: its own last / first rows
+  cuda_check(cudaMemcpy2DAsync(top, hp * 4, cur + size_t(h - trows) * pitch, pitch * 4, size_t(w) * 4, trows,
+                               cudaMemcpyDeviceToDevice, st), "halo wrap");
+  cuda_check(cudaMemcpy2DAsync(bottom, hp * 4, cur, pitch * 4, size_t(w) * 4, brows, cudaMemcpyDeviceToDevice, st),
+             "halo wrap");
+}
+
+void forward_mallat_strip(const dwt2d_plan& p, const float* strip, size_t pitch, int W, int H, int levels,
+                          float* out, size_t op, float* ws, dwt2d_halo_fn ex, void* user, cudaStream_t st) {
+  const size_t hp = strip_pitch(W);
+  float* top = ws + ll_offset(W, H, levels + 1);
+  float* bottom = top + strip_halo_rows(p) * hp;
+  const float* cur = strip;
+  size_t cur_pitch = pitch;
+  int l = 1;
+  const char* env = std::getenv("DWT2D_PAIR");
+  if (levels >= 2 && pair_capable(p) && !(env && *env == '0') && W % 16 == 0 && H % 4 == 0) {
+    const int w2 = W / 2, h2 = H / 2, w4 = W / 4, h4 = H / 4;
+    gpu::PairArgs t{};
+    gpu::LevelArgs& a = t.l1;
+    float* const d1[3] = {out + w2, out + size_t(h2) * op, out + size_t(h2) * op + w2};
+    float* ll2 = levels == 2 ? out : ll_slot(ws, W, H, 2);
+    const size_t ll2p = levels == 2 ? op : size_t(w4);
+    float* const d2[4] = {ll2, out + w4, out + size_t(h4) * op, out + size_t(h4) * op + w4};
+    for (int j = 0; j < 4; ++j) {
+      a.in[j] = cur, a.in_pitch[j] = (long long)cur_pitch;
+      a.halo_top[j] = top, a.halo_bot[j] = bottom;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)hp;
+      a.out[j] = d1[j == 0 ? 0 : j - 1], a.out_pitch[j] = (long long)op;
+      t.l2.in[j] = cur, t.l2.in_pitch[j] = (long long)cur_pitch;
+      t.l2.out[j] = d2[j], t.l2.out_pitch[j] = (long long)(j == 0 ? ll2p : op);
+    }
+    a.halo = 1, a.up = 3 * p.up, a.down = 3 * p.down;
+    a.w2 = w2, a.h2 = h2;
+    t.l2.w2 = w4, t.l2.h2 = h4;
+    prepare(p, t.l1, kFromImage);
+    prepare(p, t.l2, kFromImage);
+    if (t.l1.vec && t.l2.vec && 2 * a.up <= H && 2 * a.down <= H) {
+      strip_exchange(ex, user, cur, cur_pitch, W, H, top, bottom, hp, 2 * a.up, 2 * a.down, st);
+      run_pair(p, t, st);
+      cur = ll2, cur_pitch = ll2p, l = 3;
+    }
+  }
+  for (; l <= levels; ++l) {
+    const int w = W >> (l - 1), h = H >> (l - 1), w2 = w / 2, h2 = h / 2;
+    float* ll = l == levels ? out : ll_slot(ws, W, H, l);
+    const size_t llp = l == levels ? op : size_t(w2);
+    strip_exchange(ex, user, cur, cur_pitch, w, h, top, bottom, hp, 2 * p.up, 2 * p.down, st);
+    gpu::LevelArgs a{};
+    fill_forward_level(a, cur, cur_pitch, ll, llp, out, op, w2, h2);
+    for (int j = 0; j < 4; ++j) {
+      a.halo_top[j] = top, a.halo_bot[j] = bottom;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)hp;
+    }
+    a.halo = 1, a.up = p.up, a.down = p.down;
+    launch(p, a, kFromImage, st);
+    cur = ll, cur_pitch = llp;
+  }
+}
+
 // ------------------------------------------------- host end-to-end pipeline
 //
 // Host image -> Mallat pyramid -> host, with the transfers overlapped with
@@ -1195,6 +1278,40 @@ int dwt2d_forward_level_strip(const dwt2d_plan* p, const float* image, size_t pi
 }
 
 int dwt2d_plan_has_pair(const dwt2d_plan* p) { return p && pair_capable(*p) ? 1 : 0; }
+
+size_t dwt2d_strip_workspace_bytes(const dwt2d_plan* p, int width, int height, int levels) {
+  if (!p || width <= 0 || height <= 0 || levels < 1) return 0;
+  return strip_workspace_floats(*p, width, height, levels) * sizeof(float);
+}
+
+int dwt2d_forward_mallat_strip(const dwt2d_plan* p, const float* strip, size_t pitch, int W, int H, int levels,
+                               float* out, size_t out_pitch, void* scratch, dwt2d_halo_fn exchange, void* user,
+                               void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!strip || !out) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat_strip: plan is an inverse plan");
+    check_pyramid(W, H, levels);
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (p->extension != DWT2D_PERIODIC) fail(DWT2D_EUNSUPPORTED, "row strips need periodic extension");
+    const cudaStream_t st = as_stream(stream);
+    float* ws = static_cast<float*>(scratch);
+    void* owned = nullptr;
+    if (!ws) {
+      cuda_check(cudaMallocAsync(&owned, strip_workspace_floats(*p, W, H, levels) * sizeof(float), st),
+                 "strip workspace");
+      ws = static_cast<float*>(owned);
+    }
+    struct Free {
+      void* m;
+      cudaStream_t s;
+      ~Free() {
+        if (m) cudaFreeAsync(m, s);
+      }
+    } free_ws{owned, st};
+    forward_mallat_strip(*p, strip, pitch, W, H, levels, out, out_pitch, ws, exchange, user, st);
+  });
+}
 
 int dwt2d_forward_pair_strip(const dwt2d_plan* p, const float* image, size_t pitch, int width, int height,
                              const float* top, const float* bottom, size_t halo_pitch, float* const out1[3],

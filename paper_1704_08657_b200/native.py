@@ -72,6 +72,9 @@ _sz = ctypes.c_size_t
 _fp = ctypes.POINTER(ctypes.c_float)
 _P4 = ctypes.c_void_p * 4
 _S4 = ctypes.c_size_t * 4
+# dwt2d_halo_fn (include/dwt2d_b200.h)
+HaloFn = ctypes.CFUNCTYPE(ctypes.c_int, _p, _p, _sz, ctypes.c_int, ctypes.c_int, _p, _p, _sz, ctypes.c_int,
+                          ctypes.c_int, _p)
 _P3 = ctypes.c_void_p * 3
 _S3 = ctypes.c_size_t * 3
 
@@ -90,6 +93,9 @@ _SIGS = {
     "dwt2d_forward_level_strip": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, _p, _p, _sz, _P4,
                                                  _S4, _p]),
     "dwt2d_plan_has_pair": (ctypes.c_int, [_p]),
+    "dwt2d_strip_workspace_bytes": (_sz, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "dwt2d_forward_mallat_strip": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
+                                                  _p, _p, _p, _p]),
     "dwt2d_forward_pair_strip": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, _p, _p, _sz, _P3, _S3,
                                                 _P4, _S4, _p]),
     "dwt2d_inverse_level_strip": (ctypes.c_int, [_p, _P4, _S4, _P4, _P4, _S4, _p, _sz, ctypes.c_int,

@@ -44,16 +44,22 @@ class HaloExchange:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
 
-    def __call__(self, strip, top_rows: int, bottom_rows: int):
+    def __call__(self, strip, top_rows: int, bottom_rows: int, top=None, bottom=None):
         """Returns (top, bottom): the rows above and below `strip` in the
-        global (periodic) image."""
+        global (periodic) image, received into `top`/`bottom` if given."""
         if self.world == 1:  # periodic wrap of the only strip
-            return strip[-top_rows:], strip[:bottom_rows]
+            if top is None:
+                return strip[-top_rows:], strip[:bottom_rows]
+            top.copy_(strip[-top_rows:])
+            bottom.copy_(strip[:bottom_rows])
+            return top, bottom
         import torch
         dist = self.dist
         prev, nxt = ring_neighbours(self.rank, self.world)
-        top = torch.empty((top_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
-        bottom = torch.empty((bottom_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        if top is None:
+            top = torch.empty((top_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        if bottom is None:
+            bottom = torch.empty((bottom_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
         # Post order matters when prev == next (2 ranks): messages between one
         # pair of ranks match in posting order, so sends go [to prev: my first
         # rows, to next: my last rows] and receives [from next: bottom, from
@@ -73,13 +79,31 @@ class HaloExchange:
 LevelFn = Callable[[object, object, object], Sequence[object]]
 
 
+def _call(fn, cur, top, bottom, outs):
+    """Run a level (pair) function writing into `outs` when it accepts an
+    `out=` argument (the GPU functions do: bands land in the Mallat buffer
+    without a copy); otherwise copy its result in."""
+    try:
+        res = fn(cur, top, bottom, out=outs)
+    except TypeError:
+        res = fn(cur, top, bottom)
+    return res
+
+
+def _place(dst, src):
+    if dst.data_ptr() != src.data_ptr():
+        dst.copy_(src)
+
+
 def forward_mallat_strips(level_fn: LevelFn, strip, levels: int, up: int, down: int,
                           exchange: Callable, out=None, pair_fn: Callable | None = None):
-    """Strip-sharded forward pyramid. level_fn(strip, top, bottom) returns
-    the strip's four bands (LL, HL, LH, HH). pair_fn(strip, top, bottom), if
-    given, runs levels 1 and 2 in one pass from 6*up / 6*down halo rows and
-    returns ([HL1, LH1, HH1], [LL2, HL2, LH2, HH2]). Works on torch tensors
-    (CPU or CUDA). Returns the rank's strip-Mallat buffer."""
+    """Strip-sharded forward pyramid. level_fn(strip, top, bottom[, out])
+    returns the strip's four bands (LL, HL, LH, HH). pair_fn(strip, top,
+    bottom[, out]), if given, runs levels 1 and 2 in one pass from 6*up /
+    6*down halo rows and returns ([HL1, LH1, HH1], [LL2, HL2, LH2, HH2]).
+    Functions that take `out=` write the detail bands straight into their
+    quadrants of the strip-Mallat buffer. Works on torch tensors (CPU or
+    CUDA). Returns the rank's strip-Mallat buffer."""
     import torch
     h0, w0 = strip.shape
     if out is None:
@@ -90,29 +114,26 @@ def forward_mallat_strips(level_fn: LevelFn, strip, levels: int, up: int, down: 
         h, w = cur.shape
         check_strip(h, w, 3 * up, 3 * down)
         top, bottom = exchange(cur, 6 * up, 6 * down)
-        (hl1, lh1, hh1), (ll2, hl2, lh2, hh2) = pair_fn(cur, top, bottom)
         h2, w2, h4, w4 = h // 2, w // 2, h // 4, w // 4
-        out[:h2, w2:w] = hl1
-        out[h2:h, :w2] = lh1
-        out[h2:h, w2:w] = hh1
-        out[:h4, w4:w2] = hl2
-        out[h4:h2, :w4] = lh2
-        out[h4:h2, w4:w2] = hh2
-        if levels == 2:
-            out[:h4, :w4] = ll2
+        ll2 = out[:h4, :w4] if levels == 2 else torch.empty((h4, w4), dtype=strip.dtype, device=strip.device)
+        o1 = [out[:h2, w2:w], out[h2:h, :w2], out[h2:h, w2:w]]
+        o2 = [ll2, out[:h4, w4:w2], out[h4:h2, :w4], out[h4:h2, w4:w2]]
+        r1, r2 = _call(pair_fn, cur, top, bottom, (o1, o2))
+        for d, s_ in zip(o1 + o2, list(r1) + list(r2)):
+            _place(d, s_)
         cur, first = ll2, 2
     for lvl in range(first, levels):
         h, w = cur.shape
         check_strip(h, w, up, down)
         top, bottom = exchange(cur, 2 * up, 2 * down)
-        ll, hl, lh, hh = level_fn(cur, top, bottom)
         h2, w2 = h // 2, w // 2
-        out[:h2, w2:w] = hl
-        out[h2:h, :w2] = lh
-        out[h2:h, w2:w] = hh
+        last = lvl == levels - 1
+        ll = out[:h2, :w2] if last else torch.empty((h2, w2), dtype=strip.dtype, device=strip.device)
+        outs = [ll, out[:h2, w2:w], out[h2:h, :w2], out[h2:h, w2:w]]
+        res = _call(level_fn, cur, top, bottom, outs)
+        for d, s_ in zip(outs, res):
+            _place(d, s_)
         cur = ll
-        if lvl == levels - 1:
-            out[:h2, :w2] = ll
     return out
 
 
@@ -141,9 +162,17 @@ def assemble_mallat(strips: Sequence, levels: int):
 
 def gpu_level_fn(plan, stream=None) -> LevelFn:
     """The product's level function: the fused sm_100a kernel with halo rows."""
-    def fn(cur, top, bottom):
-        return plan.forward_level_strip(cur, top, bottom, stream=stream)
+    def fn(cur, top, bottom, out=None):
+        return plan.forward_level_strip(cur, top, bottom, out=out, stream=stream)
     return fn
+
+
+def gpu_forward_mallat(plan, strip, levels: int, exchange=None, out=None, scratch=None, stream=None):
+    """The product's strip pyramid: the C++ driver (dwt2d_forward_mallat_strip)
+    runs every level (levels 1+2 fused where the plan has the pair kernel)
+    and calls back into `exchange` (e.g. a HaloExchange) for the halo rows."""
+    ex = None if exchange is None else (lambda cur, tr, br, top, bottom: exchange(cur, tr, br, top, bottom))
+    return plan.forward_mallat_strip(strip, levels, exchange=ex, out=out, scratch=scratch, stream=stream)
 
 
 def gpu_pair_fn(plan, stream=None):
@@ -151,6 +180,6 @@ def gpu_pair_fn(plan, stream=None):
     if not plan.has_pair:
         return None
 
-    def fn(cur, top, bottom):
-        return plan.forward_pair_strip(cur, top, bottom, stream=stream)
+    def fn(cur, top, bottom, out=None):
+        return plan.forward_pair_strip(cur, top, bottom, out=out, stream=stream)
     return fn

@@ -35,6 +35,19 @@ def _dev(t, name="tensor"):
     return t.data_ptr(), (t.stride(0) if t.size(0) > 1 else t.size(1))
 
 
+class _CudaView:
+    """A device pointer as a __cuda_array_interface__ object (zero-copy)."""
+
+    def __init__(self, ptr, rows, cols, pitch):
+        self.__cuda_array_interface__ = {"shape": (rows, cols), "strides": (pitch * 4, 4), "typestr": "<f4",
+                                         "data": (ptr, False), "version": 3, "stream": None}
+
+
+def _wrap(ptr, rows, cols, pitch, device):
+    import torch
+    return torch.as_tensor(_CudaView(ptr, rows, cols, pitch), device=device)
+
+
 class Plan:
     """A compiled transform plan (forward scheme or inverse lifting)."""
 
@@ -151,20 +164,57 @@ class Plan:
                                                 N._P4(*optr), N._S4(*opit), _stream_handle(stream)))
         return list(out)
 
+    def forward_mallat_strip(self, strip, levels: int, exchange=None, out=None, scratch=None, stream=None):
+        """Whole forward pyramid of a row strip in the library (C++ driver,
+        dwt2d_forward_mallat_strip): `exchange(cur, top_rows, bottom_rows,
+        top, bottom)` fills the device tensors `top`/`bottom` with the rows
+        above/below the level input `cur` in the global image (e.g.
+        strips.HaloExchange); None = the strip is the whole periodic image.
+        Returns the strip-Mallat buffer."""
+        import torch
+        H, W = strip.shape
+        if out is None:
+            out = torch.empty((H, W), dtype=torch.float32, device=strip.device)
+        ptr, pitch = _dev(strip, "strip")
+        optr, opitch = _dev(out, "out")
+        if scratch is None:
+            nbytes = N.lib.dwt2d_strip_workspace_bytes(self._h, W, H, levels)
+            scratch = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=strip.device)
+        cb = None
+        if exchange is not None:
+            def _cb(user, cur, cpitch, w, h, top, bottom, hpitch, trows, brows, st):
+                try:
+                    dev = strip.device
+                    exchange(_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
+                             _wrap(bottom, brows, w, hpitch, dev))
+                    return 0
+                except Exception:  # surfaced as DWT2D_EINVAL by the library
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            cb = N.HaloFn(_cb)
+        N.check(N.lib.dwt2d_forward_mallat_strip(self._h, ptr, pitch, W, H, levels, optr, opitch,
+                                                 scratch.data_ptr(), cb, None, _stream_handle(stream)))
+        return out
+
     @property
     def has_pair(self) -> bool:
         """Whether levels 1 and 2 can run fused (forward_pair_strip)."""
         return bool(N.lib.dwt2d_plan_has_pair(self._h))
 
-    def forward_pair_strip(self, strip, top, bottom, stream=None):
+    def forward_pair_strip(self, strip, top, bottom, out=None, stream=None):
         """Levels 1 and 2 of a row strip in one pass; `top`/`bottom` are the
-        6*reach_up / 6*reach_down image rows above/below it. Returns
-        (level-1 [HL, LH, HH], level-2 [LL, HL, LH, HH])."""
+        6*reach_up / 6*reach_down image rows above/below it. Returns (and
+        writes into `out`, if given: pitched views are fine) (level-1 [HL,
+        LH, HH], level-2 [LL, HL, LH, HH])."""
         import torch
         H, W = strip.shape
         d = strip.device
-        out1 = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=d) for _ in range(3)]
-        out2 = [torch.empty((H // 4, W // 4), dtype=torch.float32, device=d) for _ in range(4)]
+        if out is None:
+            out1 = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=d) for _ in range(3)]
+            out2 = [torch.empty((H // 4, W // 4), dtype=torch.float32, device=d) for _ in range(4)]
+        else:
+            out1, out2 = out
         ptr, pitch = _dev(strip, "strip")
         tptr, tpitch = _dev(top, "top")
         bptr, bpitch = _dev(bottom, "bottom")

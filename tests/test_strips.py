@@ -154,3 +154,54 @@ def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme
     assert not errors, errors
     g = S.assemble_mallat(outs, L)
     assert torch.equal(g, full.cpu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
+                                                ("cdf53", "separable-lifting", False),
+                                                ("dd137", "nonseparable-lifting", True)])
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, pair, monkeypatch):
+    """The C++ strip-pyramid driver (dwt2d_forward_mallat_strip) with a
+    Python halo-exchange callback reproduces the single-GPU pyramid bit for
+    bit: world 1 without a callback (periodic wrap inside the strip), 2 and
+    4 virtual ranks as threads; with and without the fused level pair."""
+    import paper_1704_08657_b200 as dwt
+    monkeypatch.setenv("DWT2D_PAIR", pair)
+    plan = dwt.Plan(wavelet, scheme, optimized=opt)
+    W, Hs, L = 256, 128, 4
+    img = torch.from_numpy(O.random_image(W, Hs * world, 3)).to(cuda)
+    full = plan.forward_mallat(img, L)
+    if world == 1:
+        got = S.gpu_forward_mallat(plan, img, L)
+        torch.cuda.synchronize()
+        assert torch.equal(got, full)
+        return
+    ring = VirtualRing(world)
+    outs = [None] * world
+    errors = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(cuda)
+            ex = ring.exchange_for(rank)
+
+            def fill(cur, tr, br, top, bottom):
+                t, b = ex(cur, tr, br)
+                top.copy_(t)
+                bottom.copy_(b)
+            strip = img[rank * Hs:(rank + 1) * Hs].contiguous()
+            outs[rank] = S.gpu_forward_mallat(plan, strip, L, exchange=fill)
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            errors.append(e)
+            ring.barrier.abort()
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert torch.equal(S.assemble_mallat(outs, L), full.cpu())
