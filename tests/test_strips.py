@@ -26,6 +26,25 @@ def oracle_level_fn(wavelet, scheme, opt, up, down):
     return fn
 
 
+def oracle_pair_fn(wavelet, scheme, opt, up, down):
+    """Levels 1 and 2 of the float64 oracle on [top; strip; bottom] with the
+    fused pair's 6*up / 6*down halo rows, cropped to the strip's rows."""
+    def fn(cur, top, bottom):
+        tall = torch.cat([top, cur, bottom]).double().numpy()
+        r1 = O.transform(wavelet, scheme, O.split(tall), opt)
+        h2 = cur.shape[0] // 2
+        det1 = [torch.from_numpy(np.ascontiguousarray(r[3 * up:3 * up + h2])) for r in r1[1:]]
+        ll1 = r1[0]
+        s0 = (3 * up) % 2  # first LL_1 row of an even global row
+        n = ll1.shape[0] - s0
+        ll1 = ll1[s0:s0 + n - n % 2]
+        r2 = O.transform(wavelet, scheme, O.split(ll1), opt)
+        o2 = (3 * up - s0) // 2
+        lvl2 = [torch.from_numpy(np.ascontiguousarray(r[o2:o2 + h2 // 2])) for r in r2]
+        return det1, lvl2
+    return fn
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -38,13 +57,13 @@ def _worker(rank, world, port, args, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        wavelet, scheme, opt, W, Hs, levels = args
+        wavelet, scheme, opt, W, Hs, levels, pair = args
         img = O.random_image(W, Hs * world, 1, np.float64)
         strip = torch.from_numpy(img[rank * Hs:(rank + 1) * Hs].copy())
-        out = S.forward_mallat_strips(oracle_level_fn(wavelet, scheme, opt, 2 if wavelet == "cdf97" else 1,
-                                                      2 if wavelet == "cdf97" else 1),
-                                      strip, levels, 2 if wavelet == "cdf97" else 1,
-                                      2 if wavelet == "cdf97" else 1, S.HaloExchange())
+        r = 2 if wavelet == "cdf97" else 1
+        out = S.forward_mallat_strips(oracle_level_fn(wavelet, scheme, opt, r, r), strip, levels, r, r,
+                                      S.HaloExchange(),
+                                      pair_fn=oracle_pair_fn(wavelet, scheme, opt, r, r) if pair else None)
         gathered = [torch.empty_like(out) for _ in range(world)]
         dist.all_gather(gathered, out)
         if rank == 0:
@@ -58,12 +77,16 @@ def _worker(rank, world, port, args, q):
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
                                                 ("cdf53", "separable-lifting", False)])
-def test_gloo_strip_pyramid_equals_full_image(world, wavelet, scheme, opt):
+@pytest.mark.parametrize("pair", [False, True])
+def test_gloo_strip_pyramid_equals_full_image(world, wavelet, scheme, opt, pair):
+    """Strip pyramid over gloo ranks = the full-image oracle pyramid; with
+    `pair`, levels 1+2 come from one 6*up / 6*down-row halo exchange (the
+    fused level pair's data flow)."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    args = (wavelet, scheme, opt, 32, 32, 3)
+    args = (wavelet, scheme, opt, 32, 32, 3, pair)
     procs = [ctx.Process(target=_worker, args=(r, world, port, args, q)) for r in range(world)]
     for p in procs:
         p.start()
@@ -71,6 +94,16 @@ def test_gloo_strip_pyramid_equals_full_image(world, wavelet, scheme, opt):
         p.join(120)
         assert p.exitcode == 0
     assert q.get(timeout=10) < 1e-12
+
+
+def test_exchange_into_given_buffers():
+    """HaloExchange receives into caller buffers (the C++ strip driver's
+    callback contract); single rank: periodic wrap."""
+    strip = torch.arange(40.0).reshape(10, 4)
+    top, bottom = torch.empty(3, 4), torch.empty(2, 4)
+    t, b = S.HaloExchange()(strip, 3, 2, top=top, bottom=bottom)
+    assert t is top and b is bottom
+    assert torch.equal(top, strip[-3:]) and torch.equal(bottom, strip[:2])
 
 
 def test_single_rank_exchange_is_periodic_wrap():
