@@ -461,6 +461,98 @@ struct TmaRowReader {
   }
 };
 
+// Planar vector input (inverse levels: four band planes -> image) staged the
+// same way: lanes 0..3 each copy band j's 32 x CW floats of a component row
+// (one cp.async.bulk, more only across the right edge) into the stage, every
+// lane then reads its own float4 per band. CW 4 only (stage_ok plans).
+template <int CW, bool UPW>
+struct TmaPlanarReader {
+  static_assert(CW == 4, "planar staging: 4 component columns per lane");
+  static constexpr int kBandF4 = 32;          // float4 per band row of the warp
+  static constexpr int kBand = 32 * 4 * CW;   // bytes per band row of the warp
+  RowReader<CW, false, false, false, UPW> g;  // row walk of the four planes
+  float4* stage0;
+  unsigned long long* bar;
+  int xw0, first;  // first component column of lane 0 (wrapped), bytes up to the right edge
+  int issued, fetched, rows;
+  unsigned phase_bits;
+
+  __device__ __forceinline__ void issue_row(const LevelArgs& a) {
+    const int lane = threadIdx.x & 31;
+    if (issued < rows) {
+      if (lane < 4) {  // lane j copies band j
+        const int s = issued & (kStages - 1);
+        const float* row = lane == 0 ? g.rowp[0] : lane == 1 ? g.rowp[1] : lane == 2 ? g.rowp[2] : g.rowp[3];
+        const unsigned b = smem_addr(bar + s);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(4 * kBand) : "memory");
+        const unsigned dst = smem_addr(stage0 + s * 4 * kBandF4 + lane * kBandF4);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(row + xw0), "r"(first), "r"(b)
+                     : "memory");
+        if (first < kBand) {
+          for (int done = first; done < kBand;) {
+            const int bytes = min(kBand - done, a.w2 * 4);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    dst + unsigned(done)),
+                "l"(row), "r"(bytes), "r"(b)
+                : "memory");
+            done += bytes;
+          }
+        }
+      }
+      g.advance(a);
+    }
+    ++issued;
+  }
+
+  __device__ __forceinline__ void init(const LevelArgs& a, int xc, int first_row, int nrows) {
+    extern __shared__ __align__(128) unsigned char level_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    bar = reinterpret_cast<unsigned long long*>(level_smem) + warp * kStages;
+    stage0 = reinterpret_cast<float4*>(level_smem + ((kWarpsPerCta * kStages * 8 + 127) / 128) * 128) +
+             warp * kStages * 4 * kBandF4;
+    g.init(a, 0, first_row);
+    xw0 = wrap(xc - lane * CW, a.w2);
+    first = min(kBand, (a.w2 - xw0) * 4);
+    issued = fetched = 0;
+    rows = nrows;
+    phase_bits = 0;
+    if (lane == 0)
+      for (int s = 0; s < kStages; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar + s)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    for (int k = 0; k < kStages - 1; ++k) issue_row(a);
+  }
+
+  __device__ __forceinline__ void load(const LevelArgs& a, float (&d)[4][CW]) {
+    const int lane = threadIdx.x & 31;
+    const int s = fetched & (kStages - 1);
+    const unsigned b = smem_addr(bar + s), par = (phase_bits >> s) & 1u;
+    unsigned ok = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(b), "r"(par)
+          : "memory");
+    } while (!ok);
+    phase_bits ^= 1u << s;
+    const float4* src = stage0 + s * 4 * kBandF4;
+    sfor<0, 4>([&](auto J_) {
+      constexpr int j = decltype(J_)::value;
+      const float4 v = src[j * kBandF4 + lane];
+      d[j][0] = v.x, d[j][1] = v.y, d[j][2] = v.z, d[j][3] = v.w;
+    });
+    ++fetched;
+    __syncwarp();
+    issue_row(a);
+  }
+};
+
 __device__ __forceinline__ void st_vec(float* p, float4 v, bool stream) {
   if (stream) __stcs(reinterpret_cast<float4*>(p), v);
   else *reinterpret_cast<float4*>(p) = v;
@@ -667,20 +759,22 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
 // are the prefetch).
 template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool ALT, bool STAGED = false>
 __device__ __forceinline__ void level_dispatch(const LevelArgs& a, const int wid) {
-  static_assert(!STAGED || (IN_IL && VEC), "staged rows: interleaved vector input");
+  static_assert(!STAGED || VEC, "staged rows: vector input");
+  using StagedR = std::conditional_t<IN_IL, TmaRowReader<P::kCW, false>, TmaPlanarReader<P::kCW, false>>;
+  using StagedRU = std::conditional_t<IN_IL, TmaRowReader<P::kCW, true>, TmaPlanarReader<P::kCW, true>>;
   const int c = wid / a.nstrips;
   const int chunk = a.reverse ? a.nchunks - 1 - c : c;
   if constexpr (ALT) {
     if (a.alternate && (chunk & 1)) {
       if constexpr (STAGED)
-        level_item<P, 1, IN_IL, OUT_IL, VEC, COH, true, TmaRowReader<P::kCW, true>>(a, wid, chunk);
+        level_item<P, 1, IN_IL, OUT_IL, VEC, COH, true, StagedRU>(a, wid, chunk);
       else
         level_item<P, PF, IN_IL, OUT_IL, VEC, COH, true>(a, wid, chunk);
       return;
     }
   }
   if constexpr (STAGED)
-    level_item<P, 1, IN_IL, OUT_IL, VEC, COH, false, TmaRowReader<P::kCW, false>>(a, wid, chunk);
+    level_item<P, 1, IN_IL, OUT_IL, VEC, COH, false, StagedR>(a, wid, chunk);
   else
     level_item<P, PF, IN_IL, OUT_IL, VEC, COH, false>(a, wid, chunk);
 }

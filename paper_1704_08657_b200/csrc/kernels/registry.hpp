@@ -37,8 +37,8 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  if constexpr (IN_IL) {
-    if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader)
+  if constexpr (IN_IL || (OUT_IL && P::kCW == 4)) {
+    if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader / TmaPlanarReader)
       auto k = level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>;
       static const cudaError_t attr_ok =
           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<P::kCW>());

@@ -185,7 +185,8 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
     const char* env = std::getenv("DWT2D_TMA");
     const size_t bytes = size_t(a.w2) * size_t(a.h2) * 16;
     const bool force = env && *env == '2';
-    a.staged = layout == kFromImage && !(env && *env == '0') &&
+    const bool stageable = layout == kFromImage || (layout == kToImage && e.cw == 4);
+    a.staged = stageable && !(env && *env == '0') &&
                ((bytes >= (size_t(512) << 20) && e.stage_ok) || force) ? 1 : 0;
     if (a.staged && chunk_override <= 0 && !std::getenv("DWT2D_CHUNK_ROWS")) {
       const long long resident = resident_warps(p);

@@ -244,6 +244,35 @@ def test_tma_staged_rows_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("w", ["cdf97", "cdf53", "dd137"])
+def test_tma_staged_inverse_levels_bit_exact(dwt, cuda, w, monkeypatch):
+    """Inverse levels with the four band planes staged by TMA (forced with
+    DWT2D_TMA=2) give the same bits as register prefetch: narrow and wide
+    levels, ragged chunks, inverse pyramids."""
+    import torch
+    inv = dwt.Plan(w, "inverse-lifting")
+    for W, H in [(64, 40), (256, 200), (2400, 96), (1024, 1024)]:
+        planes = _to_dev(O.split(O.random_image(W, H, 21)), cuda)
+        for chunk in ["0", "5", "32"]:
+            if chunk == "0":
+                monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
+            else:
+                monkeypatch.setenv("DWT2D_CHUNK_ROWS", chunk)
+            monkeypatch.setenv("DWT2D_TMA", "0")
+            a = inv.inverse_level(planes)
+            monkeypatch.setenv("DWT2D_TMA", "2")
+            b = inv.inverse_level(planes)
+            assert torch.equal(a, b), (W, H, chunk)
+    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
+    coeffs = dwt.Plan(w, "nonseparable-lifting", optimized=True).forward_mallat(
+        torch.from_numpy(O.random_image(1024, 768, 5)).to(cuda), 5)
+    monkeypatch.setenv("DWT2D_TMA", "0")
+    a = inv.inverse_mallat(coeffs, 5)
+    monkeypatch.setenv("DWT2D_TMA", "2")
+    b = inv.inverse_mallat(coeffs, 5)
+    assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
                                      ("cdf97", "separable-lifting", True),
                                      ("cdf97", "nonseparable-polyconvolution", True)])
