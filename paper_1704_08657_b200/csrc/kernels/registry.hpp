@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <vector>
 
 #include "level_engine.cuh"
@@ -24,6 +25,20 @@ constexpr int kPrefetchRows = 2;
 // the previous level's last wave. DWT2D_PDL=0 disables it.
 bool pdl_enabled();
 
+// Opt a kernel into `bytes` of dynamic shared memory once per device (the
+// attribute is per function and device; a process may drive several GPUs).
+template <class K>
+cudaError_t allow_smem(K kernel, int bytes) {
+  static std::atomic<unsigned long long> done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_relaxed);
+  return e;
+}
+
 template <class P, bool IN_IL, bool OUT_IL>
 cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   const long long warps = (long long)a.nstrips * a.nchunks;
@@ -40,8 +55,7 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   if constexpr (IN_IL || (OUT_IL && P::kCW == 4)) {
     if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader / TmaPlanarReader)
       auto k = level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>;
-      static const cudaError_t attr_ok =
-          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<P::kCW>());
+      const cudaError_t attr_ok = allow_smem(k, staged_bytes<P::kCW>());
       if (attr_ok != cudaSuccess) return attr_ok;
       cfg.dynamicSmemBytes = staged_bytes<P::kCW>();
       return cudaLaunchKernelEx(&cfg, k, a);
@@ -67,8 +81,7 @@ cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
   const long long warps = (long long)t.nstrips * t.nchunks;
   if (warps <= 0) return cudaSuccess;
   auto k = pair_kernel<P>;
-  static const cudaError_t attr_ok =
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<4>());
+  const cudaError_t attr_ok = allow_smem(k, staged_bytes<4>());
   if (attr_ok != cudaSuccess) return attr_ok;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta));
