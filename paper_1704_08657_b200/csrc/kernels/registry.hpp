@@ -27,8 +27,9 @@ bool pdl_enabled();
 
 // Opt a kernel into `bytes` of dynamic shared memory once per device (the
 // attribute is per function and device; a process may drive several GPUs).
-template <class K>
-cudaError_t allow_smem(K kernel, int bytes) {
+// One cache per kernel: the kernel is the template argument.
+template <auto kernel>
+cudaError_t allow_smem(int bytes) {
   static std::atomic<unsigned long long> done{0};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
@@ -55,7 +56,8 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   if constexpr (IN_IL || (OUT_IL && P::kCW == 4)) {
     if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader / TmaPlanarReader)
       auto k = level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>;
-      const cudaError_t attr_ok = allow_smem(k, staged_bytes<P::kCW>());
+      const cudaError_t attr_ok =
+          allow_smem<level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>>(staged_bytes<P::kCW>());
       if (attr_ok != cudaSuccess) return attr_ok;
       cfg.dynamicSmemBytes = staged_bytes<P::kCW>();
       return cudaLaunchKernelEx(&cfg, k, a);
@@ -81,7 +83,7 @@ cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
   const long long warps = (long long)t.nstrips * t.nchunks;
   if (warps <= 0) return cudaSuccess;
   auto k = pair_kernel<P>;
-  const cudaError_t attr_ok = allow_smem(k, staged_bytes<4>());
+  const cudaError_t attr_ok = allow_smem<pair_kernel<P>>(staged_bytes<4>());
   if (attr_ok != cudaSuccess) return attr_ok;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta));
