@@ -238,7 +238,7 @@ __device__ __forceinline__ float ld1(const float* p) {
 }
 
 // COH: loads bypass the non-coherent path (needed when the input was written
-// earlier in the same launch, i.e. by a previous level of the tail kernel).
+// earlier in the same launch, i.e. by a previous level of the wavefront kernel).
 template <int CW, bool IL, bool VEC, bool COH = false, bool UPW = false>
 struct RowReader {
   static constexpr int NP = IL ? 1 : 4;  // row pointers kept
