@@ -192,6 +192,9 @@ int main() {
     const unsigned blocks = unsigned((a.nstrips * a.nchunks + 3) / 4);
     timeit("reg pf2", k_reg<1>, a, blocks, 0, out[3], &ref, host);
     timeit("prod reader", k_prod, a, blocks, staged_bytes<4>(), out[3], &ref, host);
+    // the same kernel held to 2 CTAs (8 warps) per SM by its shared memory:
+    // the level-1 streaming rate a warp-specialised level pair would keep
+    timeit("prod 2cta/SM", k_prod, a, blocks, 110 * 1024, out[3], &ref, host);
     timeit("prod kernel", level_kernel<P, 2, true, false, true>, a, blocks, staged_bytes<4>(), out[3], &ref, host);
     timeit("tma nb3", k_tma<3, 1>, a, blocks, smem(3), out[3], &ref, host);
     timeit("tma nb4", k_tma<4, 1>, a, blocks, smem(4), out[3], &ref, host);
