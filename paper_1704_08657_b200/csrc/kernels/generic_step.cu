@@ -16,6 +16,8 @@
 namespace dwt2d_b200 {
 namespace gpu {
 
+bool pdl_enabled();
+
 namespace {
 
 __device__ __forceinline__ int extend(int i, int n, int symmetric) {
@@ -47,6 +49,10 @@ struct GenericBatch {
 };
 
 __global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant__ GenericBatch b) {
+  // PDL: chains of sub-steps (symmetric border crops) overlap each launch
+  // with the previous step's tail; no-ops for a normal launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   int i = 0;
   while (i + 1 < b.n && int(blockIdx.x) >= b.first[i + 1]) ++i;
   const GenericStepArgs& a = b.r[i];
@@ -92,8 +98,16 @@ cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st
     b.first[i + 1] = b.first[i] + b.tiles_x[i] * ((a[i].h2 + 7) / 8);
   }
   if (b.first[n] == 0) return cudaSuccess;
-  generic_step_kernel<<<b.first[n], dim3(32, 8), 0, st>>>(b);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(b.first[n]));
+  cfg.blockDim = dim3(32, 8);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, generic_step_kernel, b);
 }
 
 }  // namespace gpu

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -262,8 +263,31 @@ struct Region {
 // One level on the generic executor: sub-step s reads the previous
 // sub-step's planes (double-buffered temporaries per region), like the
 // reference's run(); all regions of a sub-step go in one launch.
+// A per-thread, per-device side stream and fork/join events (symmetric
+// border crops overlap the fused kernel).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static thread_local SideStream per_dev[16];
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "device");
+  SideStream& ss = per_dev[dev & 15];
+  if (!ss.s) {
+    cuda_check(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking), "side stream");
+    cuda_check(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming), "fork event");
+    cuda_check(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming), "join event");
+  }
+  return ss;
+}
+
+// `mid`, if given, is launched on `st` concurrently with sub-steps
+// 0 .. S-2 (which then run on a side stream); the last sub-step (the only one
+// that writes the level's outputs) follows both on `st`.
 void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout,
-                         const std::vector<Region>& regions, cudaStream_t st) {
+                         const std::vector<Region>& regions, cudaStream_t st,
+                         const std::function<void()>* mid = nullptr) {
   if (a.halo) fail(DWT2D_EUNSUPPORTED, "row strips need a fused kernel (periodic built-in program)");
   if (regions.empty() || int(regions.size()) > gpu::kMaxGenericRegions) fail(DWT2D_EINVAL, "generic regions");
   keep_pool_memory();
@@ -279,8 +303,23 @@ void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
     tmp = static_cast<float*>(m);
   }
   std::vector<gpu::GenericStepArgs> g(n);
+  SideStream* side = nullptr;
+  if (mid && S > 1) {
+    side = &side_stream();
+    cuda_check(cudaEventRecord(side->fork, st), "fork");
+    cuda_check(cudaStreamWaitEvent(side->s, side->fork, 0), "fork");
+  } else if (mid) {
+    (*mid)();
+  }
   for (int s = 0; s < S; ++s) {
     const bool first = s == 0, last = s == S - 1;
+    cudaStream_t ss = st;
+    if (side && !last) ss = side->s;
+    if (side && last) {  // join: the fused kernel on `st`, the crops' earlier sub-steps on the side stream
+      (*mid)();
+      cuda_check(cudaEventRecord(side->join, side->s), "join");
+      cuda_check(cudaStreamWaitEvent(st, side->join, 0), "join");
+    }
     for (int i = 0; i < n; ++i) {
       const Region& r = regions[i];
       const size_t plane = ws_align(size_t(r.w) * size_t(r.h));
@@ -320,7 +359,7 @@ void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
         q.kx0 = 0, q.kx1 = r.w, q.ky0 = 0, q.ky1 = r.h;
       q.taps = taps;
     }
-    cuda_check(gpu::launch_generic_step(g.data(), n, st), "generic step launch");
+    cuda_check(gpu::launch_generic_step(g.data(), n, ss), "generic step launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (tmp) cuda_check(cudaFreeAsync(tmp, st), "generic temporaries");
@@ -346,14 +385,17 @@ void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStre
 void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
   const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
   if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
-  launch_fused(p, a, layout, st);
+  // the crops' intermediate sub-steps run on a side stream while the fused
+  // kernel covers the level; their last sub-step overwrites the border bands
+  // after it (16384^2 8-level symmetric pyramid: see DESIGN.md §3.1)
+  const std::function<void()> fused = [&] { launch_fused(p, a, layout, st); };
   const int w2 = a.w2, h2 = a.h2;
   run_generic_regions(p, a, layout,
                       {Region{0, 0, w2, my, 0, w2, 0, p.up},
                        Region{0, h2 - my, w2, my, 0, w2, my - p.down, my},
                        Region{0, 0, mx, h2, 0, p.left, 0, h2},
                        Region{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2}},
-                      st);
+                      st, &fused);
 }
 
 void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {
