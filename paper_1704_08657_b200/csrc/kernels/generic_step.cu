@@ -110,5 +110,109 @@ cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st
   return cudaLaunchKernelEx(&cfg, generic_step_kernel, b);
 }
 
+namespace {
+
+__global__ void __launch_bounds__(256) crop_tile_kernel(const __grid_constant__ CropTileArgs a) {
+  extern __shared__ float sm[];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  int t = blockIdx.x, r = 0;
+  while (r + 1 < a.nreg && t >= a.reg[r].tiles) t -= a.reg[r].tiles, ++r;
+  const CropRegion& c = a.reg[r];
+  // compute area of this tile (crop coordinates): [ax0, ax1) x [ay0, ay1)
+  int ax0 = 0, ax1 = c.w, ay0 = 0, ay1 = c.h, cx0 = 0, cx1 = c.w, cy0 = 0, cy1 = c.h;
+  if (c.along_x) {
+    cx0 = t * a.core, cx1 = min(c.w, cx0 + a.core);
+    ax0 = max(0, cx0 - a.mlo), ax1 = min(c.w, cx1 + a.mhi);
+  } else {
+    cy0 = t * a.core, cy1 = min(c.h, cy0 + a.core);
+    ay0 = max(0, cy0 - a.mlo), ay1 = min(c.h, cy1 + a.mhi);
+  }
+  const int aw = ax1 - ax0, ah = ay1 - ay0, area = aw * ah;
+  float* buf[2] = {sm, sm + 4 * area};
+  const int nthr = blockDim.x;
+  // sub-step 0 input: the crop's input over the area
+  for (int q = threadIdx.x; q < area; q += nthr) {
+    const int xa = q % aw, ya = q / aw;
+    const int x = c.x0 + ax0 + xa, y = c.y0 + ay0 + ya;
+    for (int j = 0; j < 4; ++j)
+      buf[0][j * area + q] = a.in_il ? a.in[0][(2ll * y + (j >> 1)) * a.in_pitch[0] + 2ll * x + (j & 1)]
+                                     : a.in[j][(long long)y * a.in_pitch[j] + x];
+  }
+  __syncthreads();
+  for (int s = 0; s < a.nsteps; ++s) {
+    const float* src = buf[s & 1];
+    float* dst = buf[(s + 1) & 1];
+    const bool last = s == a.nsteps - 1;
+    for (int q = threadIdx.x; q < area; q += nthr) {
+      const int xa = q % aw, ya = q / aw;
+      const int x = ax0 + xa, y = ay0 + ya;  // crop coordinates
+      if (last && (x < cx0 || x >= cx1 || y < cy0 || y >= cy1 || x < c.kx0 || x >= c.kx1 || y < c.ky0 ||
+                   y >= c.ky1))
+        continue;
+      for (int rr = 0; rr < 4; ++rr) {
+        const RowDesc row = a.rows[s * 4 + rr];
+        float v;
+        if (row.ident) {
+          v = src[rr * area + q];
+        } else {
+          float acc = 0.0f;
+          for (int k = row.tb; k < row.te; ++k) {
+            const TapDesc tp = a.taps[k];
+            // the crop's extension rule, then the area (values beyond a tile
+            // edge inside the crop only reach the discarded margins)
+            int xe = extend(x + tp.dm, c.w, a.symmetric) - ax0;
+            int ye = extend(y + tp.dn, c.h, a.symmetric) - ay0;
+            xe = min(max(xe, 0), aw - 1);
+            ye = min(max(ye, 0), ah - 1);
+            const float sv = src[tp.j * area + ye * aw + xe];
+            if (k == row.tb)
+              acc = tp.w == 1.0f ? sv : __fmul_rn(tp.w, sv);
+            else if (a.fma)
+              acc = __fmaf_rn(tp.w, sv, acc);
+            else
+              acc = __fadd_rn(acc, tp.w == 1.0f ? sv : __fmul_rn(tp.w, sv));
+          }
+          v = row.scale == 1.0f ? acc : __fmul_rn(acc, row.scale);
+        }
+        if (!last) {
+          dst[rr * area + q] = v;
+        } else {
+          const int gx = c.x0 + x, gy = c.y0 + y;
+          if (a.out_il)
+            a.out[0][(2ll * gy + (rr >> 1)) * a.out_pitch[0] + 2ll * gx + (rr & 1)] = v;
+          else
+            a.out[rr][(long long)gy * a.out_pitch[rr] + gx] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, cudaStream_t st) {
+  int tiles = 0;
+  for (int i = 0; i < a.nreg; ++i) tiles += a.reg[i].tiles;
+  if (tiles == 0) return cudaSuccess;
+  const int bytes = smem_floats * 4;
+  if (bytes > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(crop_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(tiles));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = size_t(bytes);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, crop_tile_kernel, a);
+}
+
 }  // namespace gpu
 }  // namespace dwt2d_b200

@@ -124,6 +124,32 @@ struct GenericStepArgs {
   RowDesc rows[4];
   const TapDesc* taps;
 };
+// All sub-steps of a program over the border crops of a symmetric level in ONE
+// launch (generic_step.cu: crop_tile_kernel): every CTA takes a tile of one
+// crop (core + margins along the crop's long side), keeps it in shared memory
+// through all sub-steps and writes the kept part of its core.
+struct CropRegion {
+  int x0, y0, w, h;        // crop on the component grid (extension at its edges)
+  int kx0, kx1, ky0, ky1;  // outputs written (crop coordinates)
+  int along_x;             // tiles run along x (row bands) or along y (column bands)
+  int tiles;
+};
+struct CropTileArgs {
+  const float* in[4];
+  long long in_pitch[4];
+  int in_il;
+  float* out[4];
+  long long out_pitch[4];
+  int out_il;
+  int nsteps, symmetric, fma;
+  int core, mlo, mhi;      // tile core length and margins along the long side
+  int nreg;
+  CropRegion reg[4];
+  const RowDesc* rows;     // nsteps * 4 (device)
+  const TapDesc* taps;     // (device)
+};
+cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, cudaStream_t st);
+
 // up to kMaxGenericRegions independent passes (same sub-step, different
 // grids) in one launch
 constexpr int kMaxGenericRegions = 4;

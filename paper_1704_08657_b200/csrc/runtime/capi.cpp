@@ -52,6 +52,7 @@ struct dwt2d_plan {
   bool generic = false;
   mutable std::once_flag dev_once;
   mutable dwt2d_b200::gpu::TapDesc* d_taps = nullptr;
+  mutable dwt2d_b200::gpu::RowDesc* d_rows = nullptr;
   // wavefront ticket lists (device), one per pyramid geometry
   struct WaveSchedule {
     std::vector<long long> key;
@@ -62,6 +63,7 @@ struct dwt2d_plan {
   mutable std::vector<WaveSchedule> wave_cache;
   ~dwt2d_plan() {
     if (d_taps) cudaFree(d_taps);
+    if (d_rows) cudaFree(d_rows);
     for (WaveSchedule& w : wave_cache)
       if (w.d) cudaFree(w.d);
   }
@@ -244,8 +246,15 @@ const gpu::TapDesc* device_taps(const dwt2d_plan& p) {
     cuda_check(cudaMalloc(&d, t.size() * sizeof(gpu::TapDesc)), "tap table allocation");
     cuda_check(cudaMemcpy(d, t.data(), t.size() * sizeof(gpu::TapDesc), cudaMemcpyHostToDevice), "tap table upload");
     p.d_taps = d;
+    std::vector<gpu::RowDesc> r;
+    for (const dwt2d_row& row : p.rows) r.push_back(gpu::RowDesc{row.identity, row.tap_begin, row.tap_end, row.scale});
+    if (r.empty()) r.push_back(gpu::RowDesc{1, 0, 0, 1.0f});
+    gpu::RowDesc* dr = nullptr;
+    cuda_check(cudaMalloc(&dr, r.size() * sizeof(gpu::RowDesc)), "row table allocation");
+    cuda_check(cudaMemcpy(dr, r.data(), r.size() * sizeof(gpu::RowDesc), cudaMemcpyHostToDevice), "row table upload");
+    p.d_rows = dr;
   });
-  if (!p.d_taps) fail(DWT2D_ECUDA, "tap table unavailable");
+  if (!p.d_taps || !p.d_rows) fail(DWT2D_ECUDA, "tap table unavailable");
   return p.d_taps;
 }
 
@@ -385,17 +394,53 @@ void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStre
 void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
   const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
   if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
-  // the crops' intermediate sub-steps run on a side stream while the fused
-  // kernel covers the level; their last sub-step overwrites the border bands
-  // after it (16384^2 8-level symmetric pyramid: see DESIGN.md §3.1)
-  const std::function<void()> fused = [&] { launch_fused(p, a, layout, st); };
   const int w2 = a.w2, h2 = a.h2;
-  run_generic_regions(p, a, layout,
-                      {Region{0, 0, w2, my, 0, w2, 0, p.up},
-                       Region{0, h2 - my, w2, my, 0, w2, my - p.down, my},
-                       Region{0, 0, mx, h2, 0, p.left, 0, h2},
-                       Region{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2}},
-                      st, &fused);
+  const char* env = std::getenv("DWT2D_CROP_TILES");
+  if (env && *env == '0') {  // one generic launch per sub-step over the four crops
+    // the crops' intermediate sub-steps run on a side stream while the fused
+    // kernel covers the level; their last sub-step overwrites the border
+    // bands after it
+    const std::function<void()> fused = [&] { launch_fused(p, a, layout, st); };
+    run_generic_regions(p, a, layout,
+                        {Region{0, 0, w2, my, 0, w2, 0, p.up},
+                         Region{0, h2 - my, w2, my, 0, w2, my - p.down, my},
+                         Region{0, 0, mx, h2, 0, p.left, 0, h2},
+                         Region{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2}},
+                        st, &fused);
+    return;
+  }
+  // all sub-steps of the four crops in one launch (crop_tile_kernel): tiles of
+  // 8 positions along each crop's long side plus margins of the program's
+  // cumulative reach, whose values only the discarded margins depend on
+  // (measured: 16384^2 symmetric pyramid 0.96 ms with 8-position tiles,
+  // 1.12 ms with 4; 4096^2 level 92 us; the per-sub-step launches: 1.22 ms /
+  // 133 us; scripts/probe_symmetric.py)
+  launch_fused(p, a, layout, st);
+  gpu::CropTileArgs t{};
+  for (int j = 0; j < 4; ++j) {
+    t.in[j] = a.in[j], t.in_pitch[j] = a.in_pitch[j];
+    t.out[j] = a.out[j], t.out_pitch[j] = a.out_pitch[j];
+  }
+  t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
+  t.nsteps = p.substeps, t.symmetric = 1, t.fma = p.fma;
+  t.core = 8;
+  if (const char* c = std::getenv("DWT2D_CROP_CORE")) t.core = std::max(1, std::atoi(c));
+  // margins: the cumulative reach toward the tile edge, plus the distance a
+  // reflection at a crop edge folds back (a reflected read near the far edge
+  // of a short last tile lands up to up+down positions inside)
+  t.mlo = t.mhi = std::max(p.left + p.right, p.up + p.down);
+  const int tx = (w2 + t.core - 1) / t.core, ty = (h2 + t.core - 1) / t.core;
+  t.nreg = 4;
+  t.reg[0] = gpu::CropRegion{0, 0, w2, my, 0, w2, 0, p.up, 1, tx};
+  t.reg[1] = gpu::CropRegion{0, h2 - my, w2, my, 0, w2, my - p.down, my, 1, tx};
+  t.reg[2] = gpu::CropRegion{0, 0, mx, h2, 0, p.left, 0, h2, 0, ty};
+  t.reg[3] = gpu::CropRegion{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2, 0, ty};
+  t.taps = device_taps(p);
+  t.rows = p.d_rows;
+  const int span = t.core + t.mlo + t.mhi;
+  const int smem_floats = 2 * 4 * std::max(my, mx) * span;
+  cuda_check(gpu::launch_crop_tiles(t, smem_floats, st), "crop tile kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void launch(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st) {

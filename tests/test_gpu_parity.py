@@ -459,12 +459,14 @@ def test_symmetric_reconstruction(dwt, cuda, w):
                                      ("cdf53", "nonseparable-polyconvolution", True),
                                      ("dd137", "nonseparable-lifting", False), ("cdf97", "inverse-lifting", False),
                                      ("dd137", "separable-lifting", True)])
-def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
+@pytest.mark.parametrize("tiles", ["1", "0"])
+def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, tiles, monkeypatch):
     """Symmetric extension on the fused kernel + generic border crops equals
     the all-generic per-step symmetric executor bit for bit: planar run(),
     forward level from the image, inverse level to the image, incl. odd
     (scalar-path) widths and grids just above the crop threshold."""
     import torch
+    monkeypatch.setenv("DWT2D_CROP_TILES", tiles)  # one tile launch, or one launch per sub-step
     fused = dwt.Plan(w, s, optimized=opt, extension="symmetric")
     monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
     gen = dwt.Plan(w, s, optimized=opt, extension="symmetric")
