@@ -62,12 +62,7 @@ struct PairArgs {
   int nstrips, chunk_rows, nchunks;
 };
 using PairLaunch = cudaError_t (*)(const PairArgs&, cudaStream_t);
-// warp-specialised pair (pair_engine.cuh: pair_ws_kernel): 4 level-1 producer
-// warps and 2 level-2 consumer warps per CTA, LL_1 rows in a shared ring
-constexpr int kWsProducers = 4, kWsConsumers = 2, kWsRing = 8;
-constexpr int kWsCols = kWsProducers * kOutLanes * 4;  // 480 LL_1 columns per CTA
-constexpr int kWsOwned = kWsCols - 16;                  // 464 columns stored per CTA
-constexpr int kWsThreads = (kWsProducers + kWsConsumers) * 32;
+
 
 // Wavefront pyramid (level_engine.cuh: wave_kernel): every level of a
 // forward pyramid in one persistent launch. `state` (device, zeroed before
@@ -102,8 +97,6 @@ struct PlanEntry {
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
   PairLaunch pair;             // levels 1+2 in one pass (forward plans with reach <= 2, CW 4)
   LevelOccupancy pair_occupancy;
-  PairLaunch pair_ws;          // the same, warp-specialised (pair_engine.cuh: pair_ws_kernel)
-  LevelOccupancy pair_ws_occupancy;
   WaveLaunch wave;             // whole forward pyramid in one launch (forward plans)
   LevelOccupancy wave_occupancy;
 };

@@ -163,215 +163,5 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) pair_kernel(const __grid_co
   pair_item<P>(t, wid % t.nstrips, wid / t.nstrips);
 }
 
-// ------------------------------------------- warp-specialised level pair
-//
-// The same two levels with the work split by warp role inside a CTA: four
-// producer warps stream level 1 (TMA-staged rows, CW 4, lanes 1..30 valid:
-// 480 LL_1 columns per CTA) and write each LL_1 row into a shared-memory ring
-// of kWsRing rows; two consumer warps run level 2 at CW 4 on the rows of that
-// ring (240 LL_1 columns = 120 level-2 columns per warp). Producers and
-// consumers hand rows over with one "full" mbarrier (4 producer arrivals) and
-// one "empty" mbarrier (2 consumer arrivals) per ring slot. The level-1
-// streaming warps never stall on level-2 arithmetic. CTAs overlap by 8 LL_1
-// columns on each side (level 2 reaches 4 LL_1 columns); each CTA stores the
-// 464 columns in the middle. Selected with DWT2D_PAIR_WS=1; bit-exact, but
-// measured slower than the one-role pair (16384^2 levels 1+2: 457 vs 422 us,
-// unchanged with a 16-row ring or sleeping waits): the ring couples the six
-// warps of a CTA into lock-step, and level-1 streaming at 8 warps/SM alone
-// already takes 348 us (scripts/tune_tma.cu).
-
-constexpr int ws_smem_bytes() { return staged_bytes<4>() + kWsRing * kWsCols * 4 + 2 * kWsRing * 8; }
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  const unsigned b = smem_addr(bar);
-  unsigned ok = 0;
-  do {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok)
-                 : "r"(b), "r"(parity)
-                 : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-template <class P>
-__device__ __forceinline__ void ws_producer(const PairArgs& t, const int X0, const int p, const int chunk, float* ringLL,
-                                            unsigned long long* full, unsigned long long* empty) {
-  using M = Meta<P>;
-  using SC = Sched<P, 1>;
-  constexpr int S = M::S, D = SC::D, UNR = SC::UNR, CW = 4, U = M::U, L = M::L;
-  const LevelArgs& a1 = t.l1;
-  const int lane = threadIdx.x & 31;
-  const int xc1 = X0 + (p * kOutLanes - 1 + lane) * CW;
-  const int m0 = chunk * t.chunk_rows, m1 = min(t.l2.h2, m0 + t.chunk_rows);
-  const int n02 = m0 - U, rows2 = (m1 - m0) + U + L;
-  const int n01 = 2 * n02 - U, rows1 = 2 * rows2 + U + L, yfirst1 = n01 - L;
-  const int iters = (rows1 + UNR - 1) / UNR * UNR;
-  const int own0 = X0 + 8;  // first stored column
-  const bool valid = lane >= 1 && lane <= kOutLanes;
-  const bool st1 = valid && xc1 >= own0 && xc1 < own0 + kWsOwned && xc1 + CW <= a1.w2;
-  float* const ring_dst = ringLL + (p * kOutLanes - 1 + lane) * CW;
-
-  float ring[S + 1][D][4][CW];
-  sfor<1, S + 1>([&](auto B_) {
-    sfor<0, D>([&](auto K_) {
-      sfor<0, 4>([&](auto J_) {
-        sfor<0, CW>([&](auto C_) {
-          ring[decltype(B_)::value][decltype(K_)::value][decltype(J_)::value][decltype(C_)::value] = 0.0f;
-        });
-      });
-    });
-  });
-  TmaRowReader<CW, false> rd;
-  rd.init(a1, xc1, n01, rows1);
-  LeanRowWriter<CW> w1;
-  w1.init(xc1, yfirst1);
-  rd.load(a1, ring[0][SC::slot(0, 0, 0)]);
-  for (int it = 0; it < iters; it += UNR) {
-    sfor<0, UNR>([&](auto U_) {
-      constexpr int u = decltype(U_)::value;
-      const int i = it + u;
-      if constexpr (!SC::kCirc) {
-        sfor<1, S + 1>([&](auto B_) {
-          constexpr int b = decltype(B_)::value;
-          constexpr int dep = SC::slots(b);
-          sfor<1, dep>([&](auto K_) {
-            constexpr int k = dep - decltype(K_)::value;
-            sfor<0, 4>([&](auto J_) {
-              sfor<0, CW>([&](auto C_) {
-                ring[b][k][decltype(J_)::value][decltype(C_)::value] =
-                    ring[b][k - 1][decltype(J_)::value][decltype(C_)::value];
-              });
-            });
-          });
-        });
-      }
-      eval_step<P, 1, 0, u, D, CW, false>(ring);
-      if (i + 1 < rows1) rd.load(a1, ring[0][SC::slot(0, u, -1)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW, false>(ring); });
-      constexpr int so = SC::slot(S, u, 0);
-      const int y1 = yfirst1 + i;
-      if (y1 >= 2 * m0 && y1 < 2 * m1 && st1) w1.template store_from<1>(a1, ring[S][so]);
-      w1.advance();
-      const int k = i - (U + L);  // LL_1 row 2 * n02 + k
-      if (k >= 0 && k < 2 * rows2) {
-        const int slot = k & (kWsRing - 1);
-        mbar_wait(empty + slot, ((k / kWsRing) & 1) ^ 1);
-        if (valid)
-          *reinterpret_cast<float4*>(ring_dst + slot * kWsCols) =
-              make_float4(ring[S][so][0][0], ring[S][so][0][1], ring[S][so][0][2], ring[S][so][0][3]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(full + slot);
-      }
-    });
-  }
-}
-
-template <class P>
-__device__ __forceinline__ void ws_consumer(const PairArgs& t, const int X0, const int c, const int chunk,
-                                            const float* ringLL, unsigned long long* full, unsigned long long* empty) {
-  using M = Meta<P>;
-  using SC = Sched<P, 1>;
-  constexpr int S = M::S, D = SC::D, UNR = SC::UNR, CW = 4, U = M::U, L = M::L;
-  const LevelArgs& a2 = t.l2;
-  const int lane = threadIdx.x & 31;
-  const int o = (c * kOutLanes - 1 + lane) * 2 * CW;  // ring column of this lane's first LL_1 column
-  const int xc2 = (X0 + o) / 2;                        // exact: X0 and o are even
-  const int m0 = chunk * t.chunk_rows, m1 = min(a2.h2, m0 + t.chunk_rows);
-  const int n02 = m0 - U, rows2 = (m1 - m0) + U + L, yfirst2 = n02 - L;
-  const int iters = (rows2 + UNR - 1) / UNR * UNR;
-  const bool inside = o >= 0 && o + 2 * CW <= kWsCols;
-  const bool valid = lane >= (c == 0 ? 2 : 1) && lane <= (c == kWsConsumers - 1 ? kOutLanes - 1 : kOutLanes);
-  const bool st2 = valid && xc2 + CW <= a2.w2;
-
-  float ring[S + 1][D][4][CW];
-  sfor<1, S + 1>([&](auto B_) {
-    sfor<0, D>([&](auto K_) {
-      sfor<0, 4>([&](auto J_) {
-        sfor<0, CW>([&](auto C_) {
-          ring[decltype(B_)::value][decltype(K_)::value][decltype(J_)::value][decltype(C_)::value] = 0.0f;
-        });
-      });
-    });
-  });
-  LeanRowWriter<CW> w2;
-  w2.init(xc2, yfirst2);
-  for (int it = 0; it < iters; it += UNR) {
-    sfor<0, UNR>([&](auto U_) {
-      constexpr int u = decltype(U_)::value;
-      const int i = it + u;
-      if (i < rows2) {
-        if constexpr (!SC::kCirc) {
-          sfor<1, S + 1>([&](auto B_) {
-            constexpr int b = decltype(B_)::value;
-            constexpr int dep = SC::slots(b);
-            sfor<1, dep>([&](auto K_) {
-              constexpr int k = dep - decltype(K_)::value;
-              sfor<0, 4>([&](auto J_) {
-                sfor<0, CW>([&](auto C_) {
-                  ring[b][k][decltype(J_)::value][decltype(C_)::value] =
-                      ring[b][k - 1][decltype(J_)::value][decltype(C_)::value];
-                });
-              });
-            });
-          });
-        }
-        // LL_1 rows 2i (ee, oe) and 2i + 1 (eo, oo) of this chunk
-        const int k0 = 2 * i, s0 = k0 & (kWsRing - 1), s1 = (k0 + 1) & (kWsRing - 1);
-        mbar_wait(full + s0, (k0 / kWsRing) & 1);
-        mbar_wait(full + s1, ((k0 + 1) / kWsRing) & 1);
-        constexpr int d0 = SC::slot(0, u, 0);
-        float4 e0 = make_float4(0.f, 0.f, 0.f, 0.f), e1 = e0, f0 = e0, f1 = e0;
-        if (inside) {
-          e0 = *reinterpret_cast<const float4*>(ringLL + s0 * kWsCols + o);
-          e1 = *reinterpret_cast<const float4*>(ringLL + s0 * kWsCols + o + 4);
-          f0 = *reinterpret_cast<const float4*>(ringLL + s1 * kWsCols + o);
-          f1 = *reinterpret_cast<const float4*>(ringLL + s1 * kWsCols + o + 4);
-        }
-        ring[0][d0][0][0] = e0.x, ring[0][d0][1][0] = e0.y, ring[0][d0][0][1] = e0.z, ring[0][d0][1][1] = e0.w;
-        ring[0][d0][0][2] = e1.x, ring[0][d0][1][2] = e1.y, ring[0][d0][0][3] = e1.z, ring[0][d0][1][3] = e1.w;
-        ring[0][d0][2][0] = f0.x, ring[0][d0][3][0] = f0.y, ring[0][d0][2][1] = f0.z, ring[0][d0][3][1] = f0.w;
-        ring[0][d0][2][2] = f1.x, ring[0][d0][3][2] = f1.y, ring[0][d0][2][3] = f1.z, ring[0][d0][3][3] = f1.w;
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(empty + s0);
-          mbar_arrive(empty + s1);
-        }
-        sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW, false>(ring); });
-        const int y2 = yfirst2 + i;
-        if (y2 >= m0 && y2 < m1 && st2) w2.template store_from<0>(a2, ring[S][SC::slot(S, u, 0)]);
-        w2.advance();
-      }
-    });
-  }
-}
-
-template <class P>
-__global__ void __launch_bounds__(kWsThreads) pair_ws_kernel(const __grid_constant__ PairArgs t) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" :::);
-  extern __shared__ __align__(128) unsigned char level_smem[];
-  float* ringLL = reinterpret_cast<float*>(level_smem + staged_bytes<4>());
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(ringLL + kWsRing * kWsCols);
-  unsigned long long* empty = full + kWsRing;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kWsRing; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(full + s)), "r"(kWsProducers) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(empty + s)), "r"(kWsConsumers) : "memory");
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5;
-  const int block = blockIdx.x % t.nstrips, chunk = blockIdx.x / t.nstrips;
-  const int X0 = block * kWsOwned - 8;
-  if (warp < kWsProducers)
-    ws_producer<P>(t, X0, warp, chunk, ringLL, full, empty);
-  else
-    ws_consumer<P>(t, X0, warp - kWsProducers, chunk, ringLL, full, empty);
-}
-
 }  // namespace gpu
 }  // namespace dwt2d_b200

@@ -99,37 +99,6 @@ cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
 }
 
 template <class P>
-cudaError_t launch_pair_ws(const PairArgs& t, cudaStream_t st) {
-  const long long blocks = (long long)t.nstrips * t.nchunks;
-  if (blocks <= 0) return cudaSuccess;
-  const cudaError_t attr_ok = allow_smem<pair_ws_kernel<P>>(ws_smem_bytes());
-  if (attr_ok != cudaSuccess) return attr_ok;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(blocks));
-  cfg.blockDim = dim3(kWsThreads);
-  cfg.dynamicSmemBytes = ws_smem_bytes();
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, pair_ws_kernel<P>, t);
-}
-
-template <class P>
-int pair_ws_occupancy() {
-  int blocks = 0;
-  cudaFuncSetAttribute(pair_ws_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, ws_smem_bytes());
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pair_ws_kernel<P>, kWsThreads, ws_smem_bytes()) !=
-      cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return blocks;
-}
-
-template <class P>
 int pair_occupancy() {
   int blocks = 0;
   cudaFuncSetAttribute(pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<4>());
@@ -176,8 +145,6 @@ PlanEntry make_entry() {
     if constexpr (PairTraits<P>::ok && P::kAlt) {
       e.pair = &launch_pair<P>;
       e.pair_occupancy = &pair_occupancy<P>;
-      e.pair_ws = &launch_pair_ws<P>;
-      e.pair_ws_occupancy = &pair_ws_occupancy<P>;
     }
     e.wave_occupancy = &wave_occupancy<P>;
   } else {

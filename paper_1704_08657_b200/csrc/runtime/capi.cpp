@@ -757,30 +757,7 @@ const unsigned long long* wave_tickets(const dwt2d_plan& p, const std::vector<gp
 // size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
 // Returns false (nothing launched) when the pair is not eligible.
 // Chunking and launch of a prepared level pair.
-void run_pair_ws(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
-  // one CTA per (block of 464 LL_1 columns, chunk of level-2 rows); whole
-  // waves of ~256-row chunks as for the one-role pair
-  t.nstrips = (t.l1.w2 + gpu::kWsOwned - 1) / gpu::kWsOwned;
-  static thread_local const gpu::PlanEntry* cached = nullptr;
-  static thread_local int per_sm = 0;
-  if (cached != p.entry) {
-    cached = p.entry;
-    per_sm = p.entry->pair_ws_occupancy ? p.entry->pair_ws_occupancy() : 0;
-  }
-  const long long resident = (long long)std::max(1, per_sm) * sm_count();
-  const long long per_wave = std::max<long long>(1, resident / t.nstrips);
-  const long long waves = std::max<long long>(1, (t.l2.h2 + 128 * per_wave) / (256 * per_wave));
-  long long chunk = (t.l2.h2 + waves * per_wave - 1) / (waves * per_wave);
-  if (const char* c = std::getenv("DWT2D_PAIR_CHUNK_ROWS")) chunk = std::max(1, std::atoi(c));
-  t.chunk_rows = int(std::min<long long>(chunk, t.l2.h2));
-  t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
-  cuda_check(p.entry->pair_ws(t, st), "warp-specialised level pair kernel launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
 void run_pair(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
-  if (const char* ws = std::getenv("DWT2D_PAIR_WS"); ws && *ws == '1' && p.entry->pair_ws)
-    return run_pair_ws(p, t, st);
   // whole waves of ~256-row chunks (measured at 16384^2: one wave of 256-row
   // chunks 432 us, 1.4 waves of 192 rows 593 us, 32-row chunks 488 us: the
   // 2(U+L)+U+L warm-up rows per chunk and partial waves both cost at 8 warps

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 import paper_1704_08657_b200 as dwt  # noqa: E402
 from paper_1704_08657_b200.synth import random_image  # noqa: E402
 
-KNOBS = ["DWT2D_PAIR_WS", "DWT2D_PAIR", "DWT2D_PAIR_DEEP", "DWT2D_PAIR_CHUNK_ROWS", "DWT2D_PDL", "DWT2D_LEVEL_CHUNK_ROWS", "DWT2D_WAVEFRONT", "DWT2D_WAVE_FROM", "DWT2D_WAVE_LAG", "DWT2D_WAVE_CHUNK_ROWS", "DWT2D_CHUNK_ROWS"]
+KNOBS = ["DWT2D_PAIR", "DWT2D_PAIR_DEEP", "DWT2D_PAIR_CHUNK_ROWS", "DWT2D_PDL", "DWT2D_LEVEL_CHUNK_ROWS", "DWT2D_WAVEFRONT", "DWT2D_WAVE_FROM", "DWT2D_WAVE_LAG", "DWT2D_WAVE_CHUNK_ROWS", "DWT2D_CHUNK_ROWS"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("settings", nargs="+")

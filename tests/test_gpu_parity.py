@@ -276,14 +276,12 @@ def test_tma_staged_inverse_levels_bit_exact(dwt, cuda, w, monkeypatch):
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
                                      ("cdf97", "separable-lifting", True),
                                      ("cdf97", "nonseparable-polyconvolution", True)])
-@pytest.mark.parametrize("ws", ["0", "1"])
-def test_level_pair_bit_exact(dwt, cuda, w, s, opt, ws, monkeypatch):
+def test_level_pair_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     """Levels 1 + 2 in one pass (LL_1 kept in registers, pair_engine.cuh;
     forced on every size with DWT2D_PAIR=2) give the same bits as one launch
     per level: narrow images (strips wrap), short images (chunks wrap
     periodically), ragged chunks, pitched input, 2..5 levels."""
     import torch
-    monkeypatch.setenv("DWT2D_PAIR_WS", ws)  # one-role or warp-specialised pair
     plan = dwt.Plan(w, s, optimized=opt)
     assert plan.info["columns_per_lane"] == 4
     for W, H, L in [(1024, 768, 5), (256, 128, 3), (2400, 96, 2), (4096, 64, 2), (64, 64, 2)]:
