@@ -341,11 +341,18 @@ def main():
     import paper_1704_08657_b200 as dwt
     from paper_1704_08657_b200.synth import random_image
 
+    # stdout carries exactly one JSON line (rank 0): everything else written
+    # to fd 1 — e.g. the "NCCL version" banner printed when the first
+    # communicator is created — goes to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     n, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sharded = n > 1 or args.sharded
     if sharded:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         if n == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
@@ -443,7 +450,7 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     if sharded:
         dist.destroy_process_group()
     return 0
