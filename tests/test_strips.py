@@ -238,3 +238,51 @@ def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme
         t.join()
     assert not errors, errors
     assert torch.equal(S.assemble_mallat(outs, L), full.cpu())
+
+
+def _gpu_worker(rank, world, port, q):
+    import torch.distributed as dist
+    import paper_1704_08657_b200 as dwt
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
+        W, Hs, L = 512, 256, 4
+        img = torch.from_numpy(O.random_image(W, Hs * world, 7)).cuda()
+        ex = S.HaloExchange()
+
+        def exchange(cur, tr, br, top, bottom):  # gloo moves host tensors
+            t, b = ex(cur.cpu(), tr, br)
+            top.copy_(t)
+            bottom.copy_(b)
+
+        out = S.gpu_forward_mallat(plan, img[rank * Hs:(rank + 1) * Hs].contiguous(), L, exchange=exchange)
+        torch.cuda.synchronize()
+        gathered = [torch.empty((Hs, W)) for _ in range(world)]
+        dist.all_gather(gathered, out.cpu())
+        if rank == 0:
+            full = plan.forward_mallat(img, L).cpu()
+            q.put(bool(torch.equal(S.assemble_mallat(gathered, L), full)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_strip_driver_across_processes(world):
+    """The C++ strip driver in separate processes (one rank each, sharing one
+    GPU) with a real torch.distributed exchange (gloo over host copies):
+    bit-identical to the single-GPU pyramid."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
