@@ -1,7 +1,11 @@
 """Symmetric-extension pyramid timing under the crop switches:
     python scripts/probe_symmetric.py  (DWT2D_CROP_TILES=0|1, DWT2D_CROP_CORE=n)"""
-import os, sys, statistics
-sys.path.insert(0, '/root/repo')
+import os
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch
 import paper_1704_08657_b200 as dwt
 from paper_1704_08657_b200.synth import random_image
