@@ -122,6 +122,15 @@ DWT2D_B200_API int dwt2d_plan_create(const dwt2d_plan_desc* desc, dwt2d_plan** p
 /* compile<float> of an arbitrary lowered program (the C++ compile() path) */
 DWT2D_B200_API int dwt2d_plan_create_from_program(const dwt2d_program* prog, dwt2d_plan** plan);
 DWT2D_B200_API void dwt2d_plan_destroy(dwt2d_plan* plan);
+/* Run-time switches of a plan (no reference counterpart: execution-policy
+ * knobs for tests and sweeps). Initialised from the DWT2D_* environment
+ * variables when the plan is created; never read on the launch path.
+ * Names: "pdl" (0/1), "chunk_rows" (0 = policy), "alternate" (0/1/2), "tma"
+ * (0 off, 1 policy, 2 forced), "pair" (0 off, 1 policy, 2 forced),
+ * "pair_chunk_rows", "crop_tiles" (0/1), "crop_core", "host_band_rows".
+ * Unknown names: DWT2D_EINVAL. Not thread-safe against concurrent launches
+ * with the same plan. */
+DWT2D_B200_API int dwt2d_plan_set_tuning(dwt2d_plan* plan, const char* name, int value);
 DWT2D_B200_API int dwt2d_plan_get_info(const dwt2d_plan* plan, dwt2d_plan_info* info);
 /* The lowered tables the plan's kernel executes (rows: nsteps*4, taps),
  * the same layout as dwt2d_program. Pass NULL buffers to query counts. */
@@ -211,8 +220,8 @@ DWT2D_B200_API int dwt2d_forward_mallat_strip(const dwt2d_plan* plan, const floa
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by
  * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL
- * bands (every level's in its own slot) and the wavefront scheduler's
- * counters: at least dwt2d_workspace_bytes() bytes, or NULL to let the library
+ * bands (every level's in its own slot): at least dwt2d_workspace_bytes()
+ * bytes, or NULL to let the library
  * take it from the stream-ordered allocator. Width and height must be
  * divisible by 2^levels. */
 DWT2D_B200_API size_t dwt2d_workspace_bytes(int width, int height, int levels);

@@ -16,8 +16,6 @@
 namespace dwt2d_b200 {
 namespace gpu {
 
-bool pdl_enabled();
-
 namespace {
 
 __device__ __forceinline__ int extend(int i, int n, int symmetric) {
@@ -87,7 +85,7 @@ __global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant
 
 }  // namespace
 
-cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st) {
+cudaError_t launch_generic_step(const GenericStepArgs* a, int n, bool pdl, cudaStream_t st) {
   if (n < 1 || n > kMaxGenericRegions) return cudaErrorInvalidValue;
   GenericBatch b{};
   b.n = n;
@@ -106,7 +104,7 @@ cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, generic_step_kernel, b);
 }
 
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(256) crop_tile_kernel(const __grid_constant__ 
 
 }  // namespace
 
-cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, cudaStream_t st) {
+cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, bool pdl, cudaStream_t st) {
   int tiles = 0;
   for (int i = 0; i < a.nreg; ++i) tiles += a.reg[i].tiles;
   if (tiles == 0) return cudaSuccess;
@@ -210,7 +208,7 @@ cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, cudaStream
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, crop_tile_kernel, a);
 }
 

@@ -238,7 +238,7 @@ __device__ __forceinline__ float ld1(const float* p) {
 }
 
 // COH: loads bypass the non-coherent path (needed when the input was written
-// earlier in the same launch, i.e. by a previous level of the wavefront kernel).
+// earlier in the same launch, i.e. by a previous level of the same kernel).
 template <int CW, bool IL, bool VEC, bool COH = false, bool UPW = false>
 struct RowReader {
   static constexpr int NP = IL ? 1 : 4;  // row pointers kept
@@ -790,103 +790,6 @@ level_kernel(const LevelArgs a) {
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
   level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && IN_IL && P::kAlt, STAGED>(a, wid);
-}
-
-// ------------------------------------------------ wavefront pyramid kernel
-//
-// A whole forward Mallat pyramid in ONE persistent launch, scheduled as a
-// dataflow wavefront instead of level after level. Work items are the same
-// (level, strip, chunk) warp items as above, four adjacent strips per CTA;
-// each CTA takes the next entry of a host-built ticket list (capi.cpp:
-// wave_schedule) with one atomicAdd when it starts. (One CTA per ticket, not
-// a persistent loop: long-lived warps that take item after item streamed
-// 15-20 % slower on B200 in every variant tried, scripts/tune_wave.cu.)
-// A level-l item may only start once the level-(l-1) chunks holding the LL
-// rows it reads (its rows plus the up/down reach, periodic wrap) are
-// complete; the ticket list puts every item after all items it depends on,
-// and tickets are taken in CTA start order, so an item that waits only waits
-// for items already running: no deadlock. The list also lags each deep item
-// about one wave of level-1 items behind its inputs, so waits are rare until
-// the final drain. Effects:
-//   * LL_l rows are consumed a few microseconds after they were written, from
-//     L2 — the next level's input never comes back from HBM;
-//   * the latency-bound deep levels run in the shadow of the bandwidth-bound
-//     level 1 instead of as a chain of small launches after it.
-// Completion is counted per (level, chunk) in strips: the producer's lanes
-// fence and the count is released after a warp barrier; consumers acquire,
-// then read with L2-coherent loads (COH).
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Level-(l-1) chunks whose LL rows level l's chunk c reads: one or two
-// contiguous ranges [lo0, hi0], [lo1, hi1] (periodic wrap); lo1 > hi1 if none.
-// Mirrored on the host by capi.cpp: wave_deps (the schedule builder).
-template <int U, int L>
-__device__ __forceinline__ void wave_deps(const LevelArgs& a, const LevelArgs& prev, int c, int& lo0, int& hi0,
-                                          int& lo1, int& hi1) {
-  const int y0 = c * a.chunk_rows, y1 = min(a.h2, y0 + a.chunk_rows);
-  const int n = prev.h2;  // LL rows of the level below (= 2 * a.h2)
-  const int span = 2 * (y1 - 1 + L) + 1 - 2 * (y0 - U);  // last - first row
-  lo1 = 1, hi1 = 0;
-  if (span + 1 >= n) {
-    lo0 = 0, hi0 = prev.nchunks - 1;
-    return;
-  }
-  const int r0 = wrap(2 * (y0 - U), n), r1 = r0 + span;
-  if (r1 < n) {
-    lo0 = r0 / prev.chunk_rows, hi0 = r1 / prev.chunk_rows;
-  } else {
-    lo0 = r0 / prev.chunk_rows, hi0 = prev.nchunks - 1;
-    lo1 = 0, hi1 = (r1 - n) / prev.chunk_rows;
-  }
-}
-
-template <class P, int PF, bool IN_IL, bool OUT_IL>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
-wave_kernel(const __grid_constant__ WaveArgs t) {
-  using M = Meta<P>;
-  __shared__ unsigned s_ticket;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned full = 0xffffffffu;
-  // dynamic block index: CTAs take tickets in the order they start, so every
-  // ticket a CTA waits for belongs to a CTA that is already running
-  if (threadIdx.x == 0) s_ticket = atomicAdd(t.state, 1u);
-  __syncthreads();
-  const unsigned ticket = s_ticket;
-  if (ticket >= unsigned(t.ntickets)) return;
-  const unsigned long long e = __ldg(t.tickets + ticket);
-  const int lvl = int(e >> 56), chunk = int(e & 0xffffffffu);
-  const int strip = int((e >> 32) & 0xffffffu) * kWarpsPerCta + warp;
-  const LevelArgs& a = t.lv[lvl];
-  if (strip >= a.nstrips) return;  // warp-uniform
-  if (lvl > 0) {
-    int lo0, hi0, lo1, hi1;
-    wave_deps<M::U, M::L>(a, t.lv[lvl - 1], chunk, lo0, hi0, lo1, hi1);
-    const unsigned need = unsigned(t.lv[lvl - 1].nstrips);
-    const unsigned* done = t.state + t.done_off[lvl - 1];
-    for (;;) {
-      bool ok = true;
-      for (int k = lo0 + lane; k <= hi0; k += 32) ok = ok && ld_acquire(done + k) >= need;
-      for (int k = lo1 + lane; k <= hi1; k += 32) ok = ok && ld_acquire(done + k) >= need;
-      if (__all_sync(full, ok)) break;
-      __nanosleep(200);
-    }
-  }
-  if constexpr (P::kAlt) {
-    if (a.alternate && (chunk & 1)) {
-      level_item<P, PF, IN_IL, OUT_IL, true, true, true>(a, strip, chunk);
-    } else {
-      level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
-    }
-  } else {
-    level_item<P, PF, IN_IL, OUT_IL, true, true, false>(a, strip, chunk);
-  }
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicAdd(t.state + t.done_off[lvl] + chunk, 1u);
 }
 
 }  // namespace gpu

@@ -39,6 +39,7 @@ struct LevelArgs {
   int reverse;          // 1: hand out chunks bottom-up (see capi.cpp forward_mallat)
   int alternate;        // 1: odd chunks stream bottom-up (shared warm-up rows hit L2)
   int staged;           // 1: interleaved input rows staged in shared memory by TMA
+  int pdl;              // host only: launch with programmatic dependent launch
   // Row strips (multi-GPU): when halo != 0, component rows above the strip
   // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from
   // halo_bot (row y - h2) instead of wrapping periodically inside the strip.
@@ -64,23 +65,6 @@ struct PairArgs {
 using PairLaunch = cudaError_t (*)(const PairArgs&, cudaStream_t);
 
 
-// Wavefront pyramid (level_engine.cuh: wave_kernel): every level of a
-// forward pyramid in one persistent launch. `state` (device, zeroed before
-// the launch) holds the ticket counter, then per level one completion counter
-// per chunk starting at done_off[l]. `tickets` (device) lists the CTA work
-// items in a dependency-respecting order: level << 56 | group << 32 | chunk,
-// where the CTA's warps take strips group * kWarpsPerCta + warp.
-constexpr int kMaxWaveLevels = 16;
-struct WaveArgs {
-  LevelArgs lv[kMaxWaveLevels];
-  int nlev;
-  int ntickets;
-  unsigned* state;
-  const unsigned long long* tickets;
-  int done_off[kMaxWaveLevels];
-};
-// launch of the wavefront kernel; grid = `blocks` CTAs (= tickets)
-using WaveLaunch = cudaError_t (*)(const WaveArgs&, int blocks, cudaStream_t);
 // resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
 using LevelOccupancy = int (*)();
 
@@ -97,8 +81,6 @@ struct PlanEntry {
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
   PairLaunch pair;             // levels 1+2 in one pass (forward plans with reach <= 2, CW 4)
   LevelOccupancy pair_occupancy;
-  WaveLaunch wave;             // whole forward pyramid in one launch (forward plans)
-  LevelOccupancy wave_occupancy;
 };
 
 // One sub-step of the generic executor (kernels/generic_step.cu). `taps`
@@ -141,12 +123,12 @@ struct CropTileArgs {
   const RowDesc* rows;     // nsteps * 4 (device)
   const TapDesc* taps;     // (device)
 };
-cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, cudaStream_t st);
+cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, bool pdl, cudaStream_t st);
 
 // up to kMaxGenericRegions independent passes (same sub-step, different
 // grids) in one launch
 constexpr int kMaxGenericRegions = 4;
-cudaError_t launch_generic_step(const GenericStepArgs* a, int n, cudaStream_t st);
+cudaError_t launch_generic_step(const GenericStepArgs* a, int n, bool pdl, cudaStream_t st);
 
 const std::vector<PlanEntry>& plan_registry();
 const PlanEntry* find_plan(unsigned long long fingerprint);

@@ -22,8 +22,8 @@ constexpr int kPrefetchRows = 2;
 // for the previous kernel in the stream (griddepcontrol.wait) before it
 // reads anything and lets the next one launch once all its own CTAs have
 // started, so consecutive levels overlap launch latency and CTA ramp-up with
-// the previous level's last wave. DWT2D_PDL=0 disables it.
-bool pdl_enabled();
+// the previous level's last wave. LevelArgs::pdl = 0 (plan tuning "pdl")
+// disables it.
 
 // Opt a kernel into `bytes` of dynamic shared memory once per device (the
 // attribute is per function and device; a process may drive several GPUs).
@@ -52,7 +52,7 @@ cudaError_t launch_level(const LevelArgs& a, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = a.pdl ? 1 : 0;
   if constexpr (IN_IL || (OUT_IL && P::kCW == 4)) {
     if (a.vec && a.staged) {  // TMA-staged rows (level_engine.cuh: TmaRowReader / TmaPlanarReader)
       auto k = level_kernel<P, kPrefetchRows, IN_IL, OUT_IL, true, true>;
@@ -94,7 +94,7 @@ cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = t.l1.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k, t);
 }
 
@@ -104,23 +104,6 @@ int pair_occupancy() {
   cudaFuncSetAttribute(pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, staged_bytes<4>());
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pair_kernel<P>, kWarpsPerCta * 32, staged_bytes<4>()) !=
       cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return blocks;
-}
-
-template <class P>
-cudaError_t launch_wave(const WaveArgs& t, int blocks, cudaStream_t st) {
-  wave_kernel<P, kPrefetchRows, true, false><<<blocks, kWarpsPerCta * 32, 0, st>>>(t);
-  return cudaGetLastError();
-}
-
-template <class P>
-int wave_occupancy() {
-  int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, wave_kernel<P, kPrefetchRows, true, false>,
-                                                    kWarpsPerCta * 32, 0) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -141,12 +124,10 @@ PlanEntry make_entry() {
   if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;
     e.occupancy = &level_occupancy<P, true, false>;
-    e.wave = &launch_wave<P>;
     if constexpr (PairTraits<P>::ok && P::kAlt) {
       e.pair = &launch_pair<P>;
       e.pair_occupancy = &pair_occupancy<P>;
     }
-    e.wave_occupancy = &wave_occupancy<P>;
   } else {
     e.to_image = &launch_level<P, false, true>;
     e.occupancy = &level_occupancy<P, false, true>;

@@ -24,14 +24,43 @@
 
 using namespace dwt2d_b200;
 
-namespace dwt2d_b200 {
-namespace gpu {
-bool pdl_enabled() {
-  const char* env = std::getenv("DWT2D_PDL");
-  return !(env && *env == '0');
+// Run-time switches of a plan. Read from the DWT2D_* environment variables
+// once, when the plan is created (tuning_from_env), and changeable per plan
+// with dwt2d_plan_set_tuning (tests, sweeps); the launch path never reads the
+// environment.
+struct Tuning {
+  int pdl = 1;              // DWT2D_PDL: programmatic dependent launch between levels
+  int chunk_rows = 0;       // DWT2D_CHUNK_ROWS: rows per warp work item (0: policy)
+  int alternate = 1;        // DWT2D_ALTERNATE: 0 off, 1 levels streaming from HBM, 2 every level
+  int tma = 1;              // DWT2D_TMA: 0 off, 1 levels >= 512 MiB, 2 every stageable level
+  int pair = 1;             // DWT2D_PAIR: 0 off, 1 where level 1 is staged, 2 forced
+  int pair_chunk_rows = 0;  // DWT2D_PAIR_CHUNK_ROWS (0: policy)
+  int crop_tiles = 1;       // DWT2D_CROP_TILES: symmetric border crops in one tile launch
+  int crop_core = 8;        // DWT2D_CROP_CORE: positions per crop tile
+  int host_band_rows = 0;   // DWT2D_HOST_BAND_ROWS: image rows per host pipeline band (0: policy)
+};
+
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
 }
-}  // namespace gpu
-}  // namespace dwt2d_b200
+Tuning tuning_from_env() {
+  Tuning t;
+  t.pdl = env_int("DWT2D_PDL", t.pdl);
+  t.chunk_rows = env_int("DWT2D_CHUNK_ROWS", t.chunk_rows);
+  t.alternate = env_int("DWT2D_ALTERNATE", t.alternate);
+  t.tma = env_int("DWT2D_TMA", t.tma);
+  t.pair = env_int("DWT2D_PAIR", t.pair);
+  t.pair_chunk_rows = env_int("DWT2D_PAIR_CHUNK_ROWS", t.pair_chunk_rows);
+  t.crop_tiles = env_int("DWT2D_CROP_TILES", t.crop_tiles);
+  t.crop_core = std::max(1, env_int("DWT2D_CROP_CORE", t.crop_core));
+  t.host_band_rows = env_int("DWT2D_HOST_BAND_ROWS", t.host_band_rows);
+  return t;
+}
+}  // namespace
+
+constexpr int kMaxDevices = 64;
 
 struct dwt2d_plan {
   std::string key;
@@ -48,24 +77,24 @@ struct dwt2d_plan {
   std::string description;
   std::vector<dwt2d_row> rows;
   std::vector<dwt2d_tap> taps;
-  // generic executor (symmetric extension, programs without an AOT kernel)
+  Tuning tune;
+  // occupancy of the plan's vector level kernel and level-pair kernel
+  // (resident CTAs per SM; 0 = not yet queried)
+  mutable std::atomic<int> occ_level{0}, occ_pair{0};
+  // generic executor (symmetric extension, programs without an AOT kernel):
+  // tap tables in device memory, one copy per device the plan runs on
   bool generic = false;
-  mutable std::once_flag dev_once;
-  mutable dwt2d_b200::gpu::TapDesc* d_taps = nullptr;
-  mutable dwt2d_b200::gpu::RowDesc* d_rows = nullptr;
-  // wavefront ticket lists (device), one per pyramid geometry
-  struct WaveSchedule {
-    std::vector<long long> key;
-    unsigned long long* d = nullptr;
-    int n = 0;
+  struct DeviceTables {
+    gpu::TapDesc* taps = nullptr;
+    gpu::RowDesc* rows = nullptr;
   };
-  mutable std::mutex wave_mu;
-  mutable std::vector<WaveSchedule> wave_cache;
+  mutable std::mutex dev_mu;
+  mutable DeviceTables dev[kMaxDevices];
   ~dwt2d_plan() {
-    if (d_taps) cudaFree(d_taps);
-    if (d_rows) cudaFree(d_rows);
-    for (WaveSchedule& w : wave_cache)
-      if (w.d) cudaFree(w.d);
+    for (DeviceTables& d : dev) {
+      if (d.taps) cudaFree(d.taps);
+      if (d.rows) cudaFree(d.rows);
+    }
   }
 };
 
@@ -111,15 +140,22 @@ int guard(F&& f) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+int current_device() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "current device");
+  if (dev < 0 || dev >= kMaxDevices) fail(DWT2D_EUNSUPPORTED, "device ordinal beyond the supported range");
+  return dev;
+}
+
+// SMs of the current device (cached per device)
 int sm_count() {
-  static const int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-      return v;
-    cudaGetLastError();
-    return 148;
-  }();
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
   return n;
 }
 
@@ -137,20 +173,16 @@ bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(
 // want the most warps (2-row chunks).
 // warps of the plan's vector level kernel that are resident at once
 long long resident_warps(const dwt2d_plan& p) {
-  static thread_local const gpu::PlanEntry* cached_entry = nullptr;
-  static thread_local int cached_blocks = 0;
-  if (cached_entry != p.entry) {
-    cached_entry = p.entry;
-    cached_blocks = p.entry->occupancy ? p.entry->occupancy() : 0;
+  int blocks = p.occ_level.load(std::memory_order_relaxed);
+  if (blocks <= 0) {
+    blocks = std::max(1, p.entry->occupancy ? p.entry->occupancy() : 2);
+    p.occ_level.store(blocks, std::memory_order_relaxed);
   }
-  return std::max(1, cached_blocks ? cached_blocks : 2) * (long long)gpu::kWarpsPerCta * sm_count();
+  return blocks * (long long)gpu::kWarpsPerCta * sm_count();
 }
 
 int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
-  if (const char* env = std::getenv("DWT2D_CHUNK_ROWS")) {
-    const int v = std::atoi(env);
-    if (v > 0) return v;
-  }
+  if (p.tune.chunk_rows > 0) return p.tune.chunk_rows;
   const long long resident = resident_warps(p);
   const long long rows_total = (long long)h2 * std::max(1, nstrips);
   const long long per_warp = (rows_total + resident - 1) / resident;
@@ -162,15 +194,10 @@ int chunk_rows_for(const dwt2d_plan& p, int h2, int nstrips) {
 enum Layout { kPlanar, kFromImage, kToImage };
 
 // Work decomposition and vector-path eligibility of one level launch.
-int alternate_chunks() {
-  const char* env = std::getenv("DWT2D_ALTERNATE");
-  if (env && *env == '0') return 0;
-  return env && *env == '2' ? 2 : 1;  // 2: also single-wave levels (tests)
-}
-
 void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_override = 0) {
   if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
-  a.alternate = alternate_chunks();
+  a.alternate = p.tune.alternate == 0 ? 0 : p.tune.alternate == 2 ? 2 : 1;  // 2: also single-wave levels (tests)
+  a.pdl = p.tune.pdl ? 1 : 0;
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
@@ -185,13 +212,12 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   // per work item costs more than it hides (16384^2 pyramid levels 2..8 +16
   // us with staging, 4096^2 single levels +4..+80 us).
   {
-    const char* env = std::getenv("DWT2D_TMA");
     const size_t bytes = size_t(a.w2) * size_t(a.h2) * 16;
-    const bool force = env && *env == '2';
+    const bool force = p.tune.tma == 2;
     const bool stageable = layout == kFromImage || (layout == kToImage && e.cw == 4);
-    a.staged = stageable && !(env && *env == '0') &&
+    a.staged = stageable && p.tune.tma != 0 &&
                ((bytes >= (size_t(512) << 20) && e.stage_ok) || force) ? 1 : 0;
-    if (a.staged && chunk_override <= 0 && !std::getenv("DWT2D_CHUNK_ROWS")) {
+    if (a.staged && chunk_override <= 0 && p.tune.chunk_rows <= 0) {
       const long long resident = resident_warps(p);
       const long long rows_total = (long long)a.h2 * a.nstrips;
       a.chunk_rows = int(std::max<long long>(8, std::min<long long>(a.h2, (rows_total + 10 * resident - 1) / (10 * resident))));
@@ -225,37 +251,39 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
 void keep_pool_memory() {
   // stream-ordered allocations (workspaces, generic temporaries) are reused
   // instead of being unmapped at every synchronisation
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~uint64_t(0);
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  });
+  static std::atomic<bool> done[kMaxDevices];
+  const int dev = current_device();
+  if (done[dev].exchange(true)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
 }
 
-const gpu::TapDesc* device_taps(const dwt2d_plan& p) {
-  std::call_once(p.dev_once, [&] {
+// The plan's tap and row tables on the current device (uploaded on first use
+// per device).
+const dwt2d_plan::DeviceTables& device_tables(const dwt2d_plan& p) {
+  const int devno = current_device();
+  std::lock_guard<std::mutex> lk(p.dev_mu);
+  dwt2d_plan::DeviceTables& dt = p.dev[devno];
+  if (!dt.taps) {
     std::vector<gpu::TapDesc> t;
     for (const dwt2d_tap& k : p.taps) t.push_back(gpu::TapDesc{k.comp, k.dm, k.dn, k.w});
     if (t.empty()) t.push_back(gpu::TapDesc{0, 0, 0, 0.0f});
     gpu::TapDesc* d = nullptr;
     cuda_check(cudaMalloc(&d, t.size() * sizeof(gpu::TapDesc)), "tap table allocation");
     cuda_check(cudaMemcpy(d, t.data(), t.size() * sizeof(gpu::TapDesc), cudaMemcpyHostToDevice), "tap table upload");
-    p.d_taps = d;
     std::vector<gpu::RowDesc> r;
     for (const dwt2d_row& row : p.rows) r.push_back(gpu::RowDesc{row.identity, row.tap_begin, row.tap_end, row.scale});
     if (r.empty()) r.push_back(gpu::RowDesc{1, 0, 0, 1.0f});
     gpu::RowDesc* dr = nullptr;
     cuda_check(cudaMalloc(&dr, r.size() * sizeof(gpu::RowDesc)), "row table allocation");
     cuda_check(cudaMemcpy(dr, r.data(), r.size() * sizeof(gpu::RowDesc), cudaMemcpyHostToDevice), "row table upload");
-    p.d_rows = dr;
-  });
-  if (!p.d_taps || !p.d_rows) fail(DWT2D_ECUDA, "tap table unavailable");
-  return p.d_taps;
+    dt.taps = d, dt.rows = dr;
+  }
+  return dt;
 }
 
 size_t ws_align(size_t floats) { return (floats + 63) & ~size_t(63); }
@@ -300,7 +328,7 @@ void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
   if (a.halo) fail(DWT2D_EUNSUPPORTED, "row strips need a fused kernel (periodic built-in program)");
   if (regions.empty() || int(regions.size()) > gpu::kMaxGenericRegions) fail(DWT2D_EINVAL, "generic regions");
   keep_pool_memory();
-  const gpu::TapDesc* taps = device_taps(p);
+  const gpu::TapDesc* taps = device_tables(p).taps;
   const int S = p.substeps;
   const int n = int(regions.size());
   std::vector<size_t> off(n + 1, 0);  // per region: 2 buffers x 4 planes
@@ -368,7 +396,7 @@ void run_generic_regions(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
         q.kx0 = 0, q.kx1 = r.w, q.ky0 = 0, q.ky1 = r.h;
       q.taps = taps;
     }
-    cuda_check(gpu::launch_generic_step(g.data(), n, ss), "generic step launch");
+    cuda_check(gpu::launch_generic_step(g.data(), n, p.tune.pdl != 0, ss), "generic step launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   if (tmp) cuda_check(cudaFreeAsync(tmp, st), "generic temporaries");
@@ -395,8 +423,7 @@ void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, 
   const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
   if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
   const int w2 = a.w2, h2 = a.h2;
-  const char* env = std::getenv("DWT2D_CROP_TILES");
-  if (env && *env == '0') {  // one generic launch per sub-step over the four crops
+  if (!p.tune.crop_tiles) {  // one generic launch per sub-step over the four crops
     // the crops' intermediate sub-steps run on a side stream while the fused
     // kernel covers the level; their last sub-step overwrites the border
     // bands after it
@@ -423,8 +450,7 @@ void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, 
   }
   t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
   t.nsteps = p.substeps, t.symmetric = 1, t.fma = p.fma;
-  t.core = 8;
-  if (const char* c = std::getenv("DWT2D_CROP_CORE")) t.core = std::max(1, std::atoi(c));
+  t.core = std::max(1, p.tune.crop_core);
   // margins: the cumulative reach toward the tile edge, plus the distance a
   // reflection at a crop edge folds back (a reflected read near the far edge
   // of a short last tile lands up to up+down positions inside)
@@ -435,11 +461,12 @@ void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, 
   t.reg[1] = gpu::CropRegion{0, h2 - my, w2, my, 0, w2, my - p.down, my, 1, tx};
   t.reg[2] = gpu::CropRegion{0, 0, mx, h2, 0, p.left, 0, h2, 0, ty};
   t.reg[3] = gpu::CropRegion{w2 - mx, 0, mx, h2, mx - p.right, mx, 0, h2, 0, ty};
-  t.taps = device_taps(p);
-  t.rows = p.d_rows;
+  const dwt2d_plan::DeviceTables& dt = device_tables(p);
+  t.taps = dt.taps;
+  t.rows = dt.rows;
   const int span = t.core + t.mlo + t.mhi;
   const int smem_floats = 2 * 4 * std::max(my, mx) * span;
-  cuda_check(gpu::launch_crop_tiles(t, smem_floats, st), "crop tile kernel launch");
+  cuda_check(gpu::launch_crop_tiles(t, smem_floats, p.tune.pdl != 0, st), "crop tile kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -485,6 +512,7 @@ void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
   p.left = prog.left, p.right = prog.right, p.up = prog.up, p.down = prog.down;
   p.extension = extension;
   p.fma = prog.fused_multiply_add ? 1 : 0;
+  p.tune = tuning_from_env();
   p.rows.clear(), p.taps.clear();
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) {
@@ -560,16 +588,13 @@ void check_pyramid(int W, int H, int levels) {
 }
 
 // Workspace layout (dwt2d_workspace_bytes): the intermediate LL band of every
-// level k = 1 .. levels-1 in its own slot (the wavefront kernel has all levels
-// in flight at once), then the wavefront's scheduling counters.
+// level k = 1 .. levels-1 in its own slot.
 size_t ll_offset(int W, int H, int k) {
   size_t off = 0;
   for (int i = 1; i < k; ++i) off += ws_align(size_t(W >> i) * size_t(H >> i));
   return off;
 }
 float* ll_slot(float* ws, int W, int H, int k) { return ws + ll_offset(W, H, k); }
-// counters: one head per level + one per chunk (chunks <= rows of the level)
-size_t wave_state_words(int H, int levels) { return ws_align(size_t(levels) + size_t(H)); }
 
 struct Workspace {
   float* ptr = nullptr;
@@ -601,39 +626,6 @@ void record(void* ev, cudaStream_t st) {
   cuda_check(cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st, flags), "event record");
 }
 
-// DWT2D_WAVEFRONT=1 runs the whole pyramid as one wavefront launch when
-// every level can take the vector path (sides divisible by 4 * 2^levels for
-// CW = 4, aligned buffers). Off by default: measured on B200 it is 3 % slower
-// than one launch per level at 16384^2: level-1 work items
-// take ~70 us, so the LL_1 rows a level-2 item reads were written too long
-// before to still be in L2, and interleaving the levels costs level 1 more
-// than it saves on the deep levels.
-// DWT2D_WAVE_FROM=k runs levels k..L as one wavefront launch after one
-// launch per level for levels 1..k-1 (the deep levels are latency bound: as
-// a wavefront, level l + 1 starts on the first LL_l rows instead of after
-// the last one).
-int wave_first_level(int levels) {
-  const char* env = std::getenv("DWT2D_WAVEFRONT");
-  if (env && *env == '1') return 1;
-  if (env && *env == '0') return 0;
-  if (const char* f = std::getenv("DWT2D_WAVE_FROM")) {
-    const int k = std::atoi(f);
-    return k >= 1 && k < levels ? k : 0;
-  }
-  return 0;
-}
-
-// Rows per work item of level l inside the wavefront (DWT2D_WAVE_CHUNK_ROWS
-// overrides the deep levels): level 1 keeps the per-level policy; deeper
-// levels use short chunks so the end-of-pyramid drain (one item per level)
-// stays short.
-int wave_chunk_rows(const dwt2d_plan& p, int l, int h2, int nstrips) {
-  if (l == 1) return chunk_rows_for(p, h2, nstrips);
-  int v = 4;
-  if (const char* env = std::getenv("DWT2D_WAVE_CHUNK_ROWS")) v = std::max(1, std::atoi(env));
-  return std::min(v, h2);
-}
-
 void fill_forward_level(gpu::LevelArgs& a, const float* cur, size_t cur_pitch, float* ll, size_t ll_pitch,
                         float* out, size_t out_pitch, int w2, int h2) {
   a = gpu::LevelArgs{};
@@ -648,114 +640,6 @@ void fill_forward_level(gpu::LevelArgs& a, const float* cur, size_t cur_pitch, f
   a.w2 = w2, a.h2 = h2;
 }
 
-// Host mirror of level_engine.cuh: wave_deps (same formula).
-void wave_deps(const gpu::LevelArgs& a, const gpu::LevelArgs& prev, int U, int L, int c, int& lo0, int& hi0,
-               int& lo1, int& hi1) {
-  const int y0 = c * a.chunk_rows, y1 = std::min(a.h2, y0 + a.chunk_rows);
-  const int n = prev.h2;
-  const int span = 2 * (y1 - 1 + L) + 1 - 2 * (y0 - U);
-  lo1 = 1, hi1 = 0;
-  if (span + 1 >= n) {
-    lo0 = 0, hi0 = prev.nchunks - 1;
-    return;
-  }
-  const int r0 = ((2 * (y0 - U)) % n + n) % n, r1 = r0 + span;
-  if (r1 < n) {
-    lo0 = r0 / prev.chunk_rows, hi0 = r1 / prev.chunk_rows;
-  } else {
-    lo0 = r0 / prev.chunk_rows, hi0 = prev.nchunks - 1;
-    lo1 = 0, hi1 = (r1 - n) / prev.chunk_rows;
-  }
-}
-
-// Ticket order of the wavefront kernel. Each level hands out its chunks as
-// n-1, 0, 1, ..., n-2 (the next level's first chunk wraps onto the last
-// one), every chunk as consecutive tickets of kWarpsPerCta strips. Level-1 chunks are
-// appended one by one; before each, every deeper level appends the chunks
-// whose inputs were appended at least `lag` tickets earlier (about one wave
-// of resident CTAs: they are then finished, or nearly, when a CTA takes
-// the dependent ticket). When level 1 is exhausted the remaining deep chunks
-// follow in dependency order. Every ticket comes after all tickets it
-// depends on, which is what makes the kernel's waits deadlock-free.
-std::vector<unsigned long long> wave_schedule(const std::vector<gpu::LevelArgs>& lv, int U, int L, long long lag) {
-  const int n = int(lv.size());
-  std::vector<std::vector<long long>> end(n);
-  for (int l = 0; l < n; ++l) end[l].assign(size_t(lv[l].nchunks), -1);
-  std::vector<int> pos(n, 0);
-  std::vector<unsigned long long> out;
-  auto chunk_at = [&](int l, int p) { return p == 0 ? lv[l].nchunks - 1 : p - 1; };
-  auto ready = [&](int l, long long need_lag) {
-    if (pos[l] >= lv[l].nchunks) return false;
-    int lo0, hi0, lo1, hi1;
-    wave_deps(lv[l], lv[l - 1], U, L, chunk_at(l, pos[l]), lo0, hi0, lo1, hi1);
-    const long long now = (long long)out.size();
-    for (int r = 0; r < 2; ++r)
-      for (int d = r ? lo1 : lo0; d <= (r ? hi1 : hi0); ++d) {
-        const long long e = end[l - 1][size_t(d)];
-        if (e < 0 || now - e < need_lag) return false;
-      }
-    return true;
-  };
-  auto emit = [&](int l) {
-    const int c = chunk_at(l, pos[l]);
-    const int groups = (lv[l].nstrips + gpu::kWarpsPerCta - 1) / gpu::kWarpsPerCta;
-    for (int g = 0; g < groups; ++g)
-      out.push_back((static_cast<unsigned long long>(l) << 56) | (static_cast<unsigned long long>(g) << 32) |
-                    static_cast<unsigned long long>(unsigned(c)));
-    end[l][size_t(c)] = (long long)out.size();
-    ++pos[l];
-  };
-  while (pos[0] < lv[0].nchunks) {
-    for (int l = n - 1; l >= 1; --l)
-      while (ready(l, lag)) emit(l);
-    emit(0);
-  }
-  for (bool more = true; more;) {
-    more = false;
-    for (int l = 1; l < n; ++l)
-      while (ready(l, 0)) emit(l), more = true;
-  }
-  for (int l = 0; l < n; ++l)
-    if (pos[l] != lv[l].nchunks) fail(DWT2D_ECUDA, "wavefront schedule incomplete");
-  return out;
-}
-
-// Device copy of the ticket list for this geometry, built and uploaded on
-// first use. Returns null (caller falls back to one launch per level) when
-// the stream is being captured and the list does not exist yet: a
-// synchronous upload cannot be captured.
-const unsigned long long* wave_tickets(const dwt2d_plan& p, const std::vector<gpu::LevelArgs>& lv, long long lag,
-                                       cudaStream_t st, int& ntickets) {
-  std::vector<long long> key{lag};
-  for (const gpu::LevelArgs& a : lv) key.insert(key.end(), {a.w2, a.h2, a.chunk_rows, a.nstrips});
-  std::lock_guard<std::mutex> lk(p.wave_mu);
-  for (const dwt2d_plan::WaveSchedule& w : p.wave_cache)
-    if (w.key == key) {
-      ntickets = w.n;
-      return w.d;
-    }
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cuda_check(cudaStreamIsCapturing(st, &cs), "capture status");
-  if (cs != cudaStreamCaptureStatusNone) return nullptr;
-  const std::vector<unsigned long long> t = wave_schedule(lv, p.entry->up, p.entry->down, lag);
-  dwt2d_plan::WaveSchedule w;
-  w.key = key;
-  w.n = int(t.size());
-  void* d = nullptr;
-  cuda_check(cudaMalloc(&d, t.size() * sizeof(unsigned long long)), "wavefront ticket allocation");
-  w.d = static_cast<unsigned long long*>(d);
-  cuda_check(cudaMemcpy(w.d, t.data(), t.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice),
-             "wavefront ticket upload");
-  p.wave_cache.push_back(std::move(w));
-  ntickets = p.wave_cache.back().n;
-  return p.wave_cache.back().d;
-}
-
-// Levels l and l + 1 in one pass (pair_engine.cuh): LL_l never goes to HBM.
-// Used for levels 1+2 where level 1 streams from HBM with TMA-staged rows
-// (>= 512 MiB). DWT2D_PAIR=0 disables it, =2 forces it for levels 1+2 on any
-// size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
-// Returns false (nothing launched) when the pair is not eligible.
 // Chunking and launch of a prepared level pair.
 void run_pair(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
   // whole waves of ~256-row chunks (measured at 16384^2: one wave of 256-row
@@ -763,17 +647,16 @@ void run_pair(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
   // 2(U+L)+U+L warm-up rows per chunk and partial waves both cost at 8 warps
   // per SM)
   t.nstrips = (t.l1.w2 + gpu::kPairLanes * 4 - 1) / (gpu::kPairLanes * 4);
-  static thread_local const gpu::PlanEntry* cached = nullptr;
-  static thread_local int per_sm = 0;
-  if (cached != p.entry) {
-    cached = p.entry;
-    per_sm = p.entry->pair_occupancy ? p.entry->pair_occupancy() : 0;
+  int per_sm = p.occ_pair.load(std::memory_order_relaxed);
+  if (per_sm <= 0) {
+    per_sm = std::max(1, p.entry->pair_occupancy ? p.entry->pair_occupancy() : 1);
+    p.occ_pair.store(per_sm, std::memory_order_relaxed);
   }
   const long long resident = (long long)std::max(1, per_sm) * gpu::kWarpsPerCta * sm_count();
   const long long per_wave = std::max<long long>(1, resident / t.nstrips);  // chunks per full wave
   const long long waves = std::max<long long>(1, (t.l2.h2 + 128 * per_wave) / (256 * per_wave));
   long long chunk = (t.l2.h2 + waves * per_wave - 1) / (waves * per_wave);
-  if (const char* c = std::getenv("DWT2D_PAIR_CHUNK_ROWS")) chunk = std::max(1, std::atoi(c));
+  if (p.tune.pair_chunk_rows > 0) chunk = p.tune.pair_chunk_rows;
   t.chunk_rows = int(std::min<long long>(chunk, t.l2.h2));
   t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
   cuda_check(p.entry->pair(t, st), "level pair kernel launch");
@@ -784,23 +667,19 @@ bool pair_capable(const dwt2d_plan& p) {
   return p.entry && p.entry->pair && p.extension == DWT2D_PERIODIC;
 }
 
-// Levels l and l + 1 in one pass (pair_engine.cuh): LL_l never goes to HBM.
-// Used for levels 1+2 where level 1 streams from HBM with TMA-staged rows
-// (>= 512 MiB). DWT2D_PAIR=0 disables it, =2 forces it for levels 1+2 on any
-// size (tests); DWT2D_PAIR_DEEP=1 also pairs deeper levels (experiment).
-// Returns false (nothing launched) when the pair is not eligible.
-bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::LevelArgs& lb, int l, cudaStream_t st) {
-  if (!pair_capable(p)) return false;
-  const char* env = std::getenv("DWT2D_PAIR");
-  if (env && *env == '0') return false;
-  const bool force = env && *env == '2';
-  const char* deep = std::getenv("DWT2D_PAIR_DEEP");
-  if (l > 1 && !(deep && *deep == '1')) return false;
+// Levels 1 and 2 in one pass (pair_engine.cuh): LL_1 never goes to HBM.
+// Used where level 1 streams from HBM with TMA-staged rows (>= 512 MiB).
+// Tuning "pair": 0 disables it, 2 forces it on any size (tests). Pairing
+// deeper levels measured no gain (levels 3+4 of 16384^2: 43.4 us vs 31.1 +
+// 12.3). Returns false (nothing launched) when the pair is not eligible.
+bool launch_pair(const dwt2d_plan& p, const gpu::LevelArgs& la, const gpu::LevelArgs& lb, cudaStream_t st) {
+  if (!pair_capable(p) || p.tune.pair == 0) return false;
+  const bool force = p.tune.pair == 2;
   gpu::PairArgs t{};
   t.l1 = la, t.l2 = lb;
   prepare(p, t.l1, kFromImage);
   prepare(p, t.l2, kFromImage);
-  if (!(t.l1.vec && t.l2.vec && (t.l1.staged || force || l > 1))) return false;
+  if (!(t.l1.vec && t.l2.vec && (t.l1.staged || force))) return false;
   run_pair(p, t, st);
   return true;
 }
@@ -820,50 +699,9 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     cur = ll;
     cur_pitch = ll_pitch;
   }
-  // levels first..levels run as one wavefront launch (first = 0: none)
-  int first = wave_first_level(levels);
-  bool wave = first > 0 && p.entry && p.entry->wave && p.extension == DWT2D_PERIODIC && levels - first + 1 >= 2 &&
-              levels - first + 1 <= gpu::kMaxWaveLevels;
-  std::vector<gpu::LevelArgs> wl;
-  if (wave) {
-    for (int l = first; l <= levels && wave; ++l) {
-      gpu::LevelArgs a = lv[l - 1];
-      prepare(p, a, kFromImage);
-      const int nstrips = a.nstrips;
-      prepare(p, a, kFromImage, wave_chunk_rows(p, l, a.h2, nstrips));
-      wave = wave && a.vec;
-      wl.push_back(a);
-    }
-  }
-  gpu::WaveArgs t{};
-  if (wave) {
-    static thread_local const gpu::PlanEntry* cached = nullptr;
-    static thread_local int per_sm = 0;
-    if (cached != p.entry) {
-      cached = p.entry;
-      per_sm = p.entry->wave_occupancy ? p.entry->wave_occupancy() : 0;
-    }
-    if (per_sm <= 0) fail(DWT2D_ECUDA, "wavefront kernel cannot be resident");
-    const int blocks = per_sm * sm_count();
-    double lag_waves = first == 1 ? 1.5 : 0.0;
-    if (const char* env = std::getenv("DWT2D_WAVE_LAG")) lag_waves = std::atof(env);
-    const long long lag = (long long)(lag_waves * blocks);
-    t.tickets = wave_tickets(p, wl, lag, st, t.ntickets);
-    wave = t.tickets != nullptr;
-  }
-  const int last_single = wave ? first - 1 : levels;
-  // tuning: DWT2D_LEVEL_CHUNK_ROWS="r1,r2,..." overrides the chunk rows of
-  // the per-level launches (0 or missing entries keep the policy)
-  std::vector<int> level_chunks;
-  if (const char* env = std::getenv("DWT2D_LEVEL_CHUNK_ROWS"))
-    for (const char* q = env; *q;) {
-      level_chunks.push_back(std::atoi(q));
-      while (*q && *q != ',') ++q;
-      if (*q == ',') ++q;
-    }
-  for (int l = 1; l <= last_single; ++l) {
-    if (l + 1 <= last_single && launch_pair(p, lv[l - 1], lv[l], l, st)) {
-      if (events) record(events[l], st), record(events[l + 1], st);
+  for (int l = 1; l <= levels; ++l) {
+    if (l == 1 && levels >= 2 && launch_pair(p, lv[0], lv[1], st)) {
+      if (events) record(events[1], st), record(events[2], st);
       ++l;
       continue;
     }
@@ -872,30 +710,9 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     // level l wrote last, which are still in L2 (LL uses normal stores, the
     // detail bands evict-first).
     a.reverse = (l % 2 == 0) ? 1 : 0;
-    if (l - 1 < int(level_chunks.size()) && level_chunks[l - 1] > 0 && p.entry && p.extension == DWT2D_PERIODIC) {
-      prepare(p, a, kFromImage, level_chunks[l - 1]);
-      cuda_check((*p.entry->from_image)(a, st), "level kernel launch");
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      if (events) record(events[l], st);
-      continue;
-    }
     launch(p, a, kFromImage, st);
     if (events) record(events[l], st);
   }
-  if (!wave) return;
-  t.nlev = int(wl.size());
-  t.state = reinterpret_cast<unsigned*>(ws + ll_offset(W, H, levels));
-  int off = 1;
-  for (int l = 0; l < t.nlev; ++l) {
-    t.lv[l] = wl[l];
-    t.done_off[l] = off;
-    off += wl[l].nchunks;
-  }
-  cuda_check(cudaMemsetAsync(t.state, 0, size_t(off) * sizeof(unsigned), st), "wavefront counters");
-  cuda_check(p.entry->wave(t, t.ntickets, st), "wavefront kernel launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (events)
-    for (int l = first; l <= levels; ++l) record(events[l], st);
 }
 
 void inverse_mallat(const dwt2d_plan& p, const float* in, size_t in_pitch, int W, int H, int levels,
@@ -962,8 +779,7 @@ void forward_mallat_strip(const dwt2d_plan& p, const float* strip, size_t pitch,
   const float* cur = strip;
   size_t cur_pitch = pitch;
   int l = 1;
-  const char* env = std::getenv("DWT2D_PAIR");
-  if (levels >= 2 && pair_capable(p) && !(env && *env == '0') && W % 16 == 0 && H % 4 == 0) {
+  if (levels >= 2 && pair_capable(p) && p.tune.pair != 0 && W % 16 == 0 && H % 4 == 0) {
     const int w2 = W / 2, h2 = H / 2, w4 = W / 4, h4 = H / 4;
     gpu::PairArgs t{};
     gpu::LevelArgs& a = t.l1;
@@ -1047,18 +863,31 @@ struct HostPipe {
   }
 };
 
+// One pipeline per thread and device: its streams and staging belong to the
+// device that was current when it was created.
 HostPipe& host_pipe() {
-  static thread_local HostPipe pipe;
-  return pipe;
+  static thread_local std::unique_ptr<HostPipe> pipes[kMaxDevices];
+  std::unique_ptr<HostPipe>& p = pipes[current_device()];
+  if (!p) p = std::make_unique<HostPipe>();
+  return *p;
 }
 
-int band_rows_for(int H, int halo_rows) {
-  int r = 0;
-  if (const char* env = std::getenv("DWT2D_HOST_BAND_ROWS")) r = std::atoi(env);
+// Row bands of the host pipeline: `n` bands of `rows` image rows, the last
+// band taking the remainder (rows <= last < 2 * rows), so every band —
+// including the last — is at least `rows` >= 4 * halo rows tall and each
+// band's bottom halo lies inside the next band (or wraps to row 0).
+struct Bands {
+  int rows, n;
+  int begin(int b) const { return b * rows; }
+  int end(int b, int H) const { return b == n - 1 ? H : (b + 1) * rows; }
+};
+Bands bands_for(const dwt2d_plan& p, int H, int halo_rows) {
+  int r = p.tune.host_band_rows;
   if (r <= 0) r = H / 16;                         // ~16 bands
   r = std::max(r, std::max(64, 4 * halo_rows));   // level-2 bands need their own halo rows
   r = (r + 3) & ~3;                               // even LL1 rows per band
-  return std::min(r, H);
+  r = std::min(r, H);
+  return Bands{r, std::max(1, H / r)};
 }
 
 // One forward level on image rows [r0, r1) of a level input `in` (w_in x
@@ -1125,15 +954,15 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
   cuda_check(cudaStreamWaitEvent(hp.up, ev_alloc), "wait");
   cuda_check(cudaStreamWaitEvent(hp.down, ev_alloc), "wait");
 
-  const int R = band_rows_for(H, std::max(U, Ld) * 2);
-  const int B = (H + R - 1) / R;
+  const Bands bands = bands_for(p, H, std::max(U, Ld) * 2);
+  const int B = bands.n;
   // upload: the image's last rows first, then the bands in order
   const size_t tail0 = size_t(H - tail_rows) * W;
   cuda_check(cudaMemcpyAsync(d_img + tail0, image + tail0, size_t(tail_rows) * W * 4, cudaMemcpyHostToDevice, hp.up),
              "H2D");
   std::vector<cudaEvent_t> up(B);
   for (int b = 0; b < B; ++b) {
-    const int r0 = b * R, r1 = std::min(H, r0 + R);
+    const int r0 = bands.begin(b), r1 = bands.end(b, H);
     const int c1 = (b == B - 1) ? std::max(r0, H - tail_rows) : r1;
     if (c1 > r0)
       cuda_check(cudaMemcpyAsync(d_img + size_t(r0) * W, image + size_t(r0) * W, size_t(c1 - r0) * W * 4,
@@ -1154,7 +983,7 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     copy();
   };
   auto level2_band = [&](int b) {
-    const int r0 = (b * R) / 2, r1 = std::min(H, b * R + R) / 2;  // LL1 rows of band b
+    const int r0 = bands.begin(b) / 2, r1 = bands.end(b, H) / 2;  // LL1 rows of band b
     band_level(p, d_ll1, size_t(w2), w2, h2, r0, r1, ll2, ll2p, d_out, size_t(W), hp.comp);
     down_after([&] { band_details_down(out, d_out, W, w2, h2, r0 / 2, (r1 - r0) / 2, hp.down); });
   };
@@ -1164,7 +993,7 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     band_level(p, d_img, size_t(W), W, H, H - 4 * U, H, ll1, ll1p, d_out, size_t(W), hp.comp);
   }
   for (int b = 0; b < B; ++b) {
-    const int r0 = b * R, r1 = std::min(H, r0 + R);
+    const int r0 = bands.begin(b), r1 = bands.end(b, H);
     cuda_check(cudaStreamWaitEvent(hp.comp, up[std::min(b + 1, B - 1)]), "wait");  // bottom halo = band b + 1
     band_level(p, d_img, size_t(W), W, H, r0, r1, ll1, ll1p, d_out, size_t(W), hp.comp);
     down_after([&] { band_details_down(out, d_out, W, W, H, r0 / 2, (r1 - r0) / 2, hp.down); });
@@ -1241,6 +1070,25 @@ int dwt2d_plan_create_from_program(const dwt2d_program* t, dwt2d_plan** out) {
 }
 
 void dwt2d_plan_destroy(dwt2d_plan* p) { delete p; }
+
+int dwt2d_plan_set_tuning(dwt2d_plan* p, const char* name, int value) {
+  return guard([&] {
+    require_plan(p);
+    if (!name) fail(DWT2D_EINVAL, "null argument");
+    const std::string n = name;
+    Tuning& t = p->tune;
+    if (n == "pdl") t.pdl = value;
+    else if (n == "chunk_rows") t.chunk_rows = value;
+    else if (n == "alternate") t.alternate = value;
+    else if (n == "tma") t.tma = value;
+    else if (n == "pair") t.pair = value;
+    else if (n == "pair_chunk_rows") t.pair_chunk_rows = value;
+    else if (n == "crop_tiles") t.crop_tiles = value;
+    else if (n == "crop_core") t.crop_core = std::max(1, value);
+    else if (n == "host_band_rows") t.host_band_rows = value;
+    else fail(DWT2D_EINVAL, "unknown tuning switch: " + n);
+  });
+}
 
 int dwt2d_plan_get_info(const dwt2d_plan* p, dwt2d_plan_info* info) {
   return guard([&] {
@@ -1458,7 +1306,7 @@ int dwt2d_inverse_level_strip(const dwt2d_plan* p, const float* const in[4], con
 
 size_t dwt2d_workspace_bytes(int width, int height, int levels) {
   if (levels < 2 || width <= 0 || height <= 0) return 0;
-  return (ll_offset(width, height, levels) + wave_state_words(height, levels)) * sizeof(float);
+  return ll_offset(width, height, levels) * sizeof(float);
 }
 
 int dwt2d_forward_mallat(const dwt2d_plan* p, const float* image, size_t pitch, int W, int H, int levels,

@@ -82,6 +82,7 @@ _SIGS = {
     "dwt2d_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(_p)]),
     "dwt2d_plan_create_from_program": (ctypes.c_int, [ctypes.POINTER(Program), ctypes.POINTER(_p)]),
     "dwt2d_plan_destroy": (None, [_p]),
+    "dwt2d_plan_set_tuning": (ctypes.c_int, [_p, ctypes.c_char_p, ctypes.c_int]),
     "dwt2d_plan_get_info": (ctypes.c_int, [_p, ctypes.POINTER(PlanInfo)]),
     "dwt2d_plan_describe": (ctypes.c_int, [_p, ctypes.c_char_p, _sz]),
     "dwt2d_plan_get_tables": (ctypes.c_int, [_p, ctypes.POINTER(Row), ctypes.c_int32, ctypes.POINTER(Tap),

@@ -56,10 +56,14 @@ class HaloExchange:
         import torch
         dist = self.dist
         prev, nxt = ring_neighbours(self.rank, self.world)
-        if top is None:
-            top = torch.empty((top_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
-        if bottom is None:
-            bottom = torch.empty((bottom_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        # receive into contiguous buffers: backends move numel() packed
+        # elements from data_ptr(), so a pitched view (the library's halo
+        # rows are w floats of a wider pitch from level 3 on) would get
+        # rows 1.. misplaced; such views are filled by a copy afterwards
+        rtop = top if top is not None and top.is_contiguous() else torch.empty(
+            (top_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
+        rbot = bottom if bottom is not None and bottom.is_contiguous() else torch.empty(
+            (bottom_rows, strip.shape[1]), dtype=strip.dtype, device=strip.device)
         # Post order matters when prev == next (2 ranks): messages between one
         # pair of ranks match in posting order, so sends go [to prev: my first
         # rows, to next: my last rows] and receives [from next: bottom, from
@@ -68,11 +72,19 @@ class HaloExchange:
         ops = [
             dist.P2POp(dist.isend, strip[:bottom_rows].contiguous(), prev, self.group),
             dist.P2POp(dist.isend, strip[-top_rows:].contiguous(), nxt, self.group),
-            dist.P2POp(dist.irecv, bottom, nxt, self.group),
-            dist.P2POp(dist.irecv, top, prev, self.group),
+            dist.P2POp(dist.irecv, rbot, nxt, self.group),
+            dist.P2POp(dist.irecv, rtop, prev, self.group),
         ]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        if top is None:
+            top = rtop
+        elif top.data_ptr() != rtop.data_ptr():
+            top.copy_(rtop)
+        if bottom is None:
+            bottom = rbot
+        elif bottom.data_ptr() != rbot.data_ptr():
+            bottom.copy_(rbot)
         return top, bottom
 
 

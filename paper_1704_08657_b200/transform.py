@@ -43,6 +43,16 @@ class _CudaView:
                                          "data": (ptr, False), "version": 3, "stream": None}
 
 
+def _check_scratch(scratch, nbytes: int, device) -> None:
+    """A caller's workspace must live on the transform's device and hold at
+    least the library's workspace size (it is written without bounds)."""
+    import torch
+    if not isinstance(scratch, torch.Tensor) or not scratch.is_cuda or scratch.device != device:
+        raise ValueError(f"scratch must be a CUDA tensor on {device}")
+    if not scratch.is_contiguous() or scratch.numel() * scratch.element_size() < nbytes:
+        raise ValueError(f"scratch must be contiguous with at least {nbytes} bytes")
+
+
 def _wrap(ptr, rows, cols, pitch, device):
     import torch
     return torch.as_tensor(_CudaView(ptr, rows, cols, pitch), device=device)
@@ -85,6 +95,13 @@ class Plan:
         if h and N is not None and getattr(N, "lib", None) is not None:
             N.lib.dwt2d_plan_destroy(h)
         self._h = None
+
+    def tune(self, **switches) -> "Plan":
+        """Set run-time switches of this plan (dwt2d_plan_set_tuning), e.g.
+        plan.tune(tma=2, chunk_rows=5). Returns the plan."""
+        for k, v in switches.items():
+            N.check(N.lib.dwt2d_plan_set_tuning(self._h, k.encode(), int(v)))
+        return self
 
     # -- introspection -------------------------------------------------
     @property
@@ -177,16 +194,21 @@ class Plan:
             out = torch.empty((H, W), dtype=torch.float32, device=strip.device)
         ptr, pitch = _dev(strip, "strip")
         optr, opitch = _dev(out, "out")
+        nbytes = N.lib.dwt2d_strip_workspace_bytes(self._h, W, H, levels)
         if scratch is None:
-            nbytes = N.lib.dwt2d_strip_workspace_bytes(self._h, W, H, levels)
             scratch = torch.empty(nbytes // 4 + 64, dtype=torch.float32, device=strip.device)
+        _check_scratch(scratch, nbytes, strip.device)
         cb = None
         if exchange is not None:
             def _cb(user, cur, cpitch, w, h, top, bottom, hpitch, trows, brows, st):
                 try:
                     dev = strip.device
-                    exchange(_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
-                             _wrap(bottom, brows, w, hpitch, dev))
+                    # the exchange's copies and P2P ops are ordered on the
+                    # library's stream `st`: after the level that wrote
+                    # `cur`, before the kernel that reads the halo rows
+                    with torch.cuda.stream(torch.cuda.ExternalStream(st, device=dev)):
+                        exchange(_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
+                                 _wrap(bottom, brows, w, hpitch, dev))
                     return 0
                 except Exception:  # surfaced as DWT2D_EINVAL by the library
                     import traceback
@@ -252,7 +274,10 @@ class Plan:
             out = torch.empty((H, W), dtype=torch.float32, device=image.device)
         ptr, pitch = _dev(image, "image")
         optr, opitch = _dev(out, "out")
-        scr = None if scratch is None else scratch.data_ptr()
+        scr = None
+        if scratch is not None:
+            _check_scratch(scratch, N.lib.dwt2d_workspace_bytes(W, H, levels), image.device)
+            scr = scratch.data_ptr()
         if events is None:
             N.check(N.lib.dwt2d_forward_mallat(self._h, ptr, pitch, W, H, levels, optr, opitch, scr,
                                                _stream_handle(stream)))
@@ -271,6 +296,8 @@ class Plan:
             image = torch.empty((H, W), dtype=torch.float32, device=coeffs.device)
         cptr, cpitch = _dev(coeffs, "coeffs")
         ptr, pitch = _dev(image, "image")
+        if scratch is not None:
+            _check_scratch(scratch, N.lib.dwt2d_workspace_bytes(W, H, levels), coeffs.device)
         N.check(N.lib.dwt2d_inverse_mallat(self._h, cptr, cpitch, W, H, levels, ptr, pitch,
                                            None if scratch is None else scratch.data_ptr(),
                                            _stream_handle(stream)))

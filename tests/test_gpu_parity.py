@@ -184,34 +184,6 @@ def test_host_entry_points_match_device(dwt, cuda):
 
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
-                                     ("dd137", "separable-convolution", True),
-                                     ("cdf97", "nonseparable-convolution", True),
-                                     ("cdf97", "nonseparable-polyconvolution", False)])
-def test_wavefront_pyramid_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
-    """The whole pyramid in one wavefront launch (levels in flight together,
-    dataflow-scheduled) gives the same bits as one launch per level, for
-    several work-item sizes incl. 1-row and ragged chunks."""
-    import torch
-    plan = dwt.Plan(w, s, optimized=opt)
-    for W, H, L, c1, cd in [(512, 384, 5, "0", "16"), (512, 384, 5, "7", "1"), (96, 64, 3, "3", "5"),
-                            (1024, 256, 6, "0", "3"), (256, 1024, 4, "1000", "1000")]:
-        img = torch.from_numpy(O.random_image(W, H, 8)).to(cuda)
-        monkeypatch.setenv("DWT2D_WAVEFRONT", "0")
-        monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
-        a = plan.forward_mallat(img, L)
-        monkeypatch.setenv("DWT2D_WAVEFRONT", "1")
-        if c1 != "0":
-            monkeypatch.setenv("DWT2D_CHUNK_ROWS", c1)
-        monkeypatch.setenv("DWT2D_WAVE_CHUNK_ROWS", cd)
-        before = dwt.launch_count()
-        for _ in range(3):  # counters are reset by every call
-            b = plan.forward_mallat(img, L)
-        torch.cuda.synchronize()
-        assert dwt.launch_count() - before == 3, (W, H, L)
-        assert torch.equal(a, b), (W, H, L, c1, cd)
-
-
-@pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
                                      ("dd137", "nonseparable-lifting", True),
                                      ("cdf97", "nonseparable-convolution", False)])
 def test_tma_staged_rows_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
@@ -225,21 +197,16 @@ def test_tma_staged_rows_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
         base = torch.from_numpy(O.random_image(W + 64, H, 9)).to(cuda)
         for img in (base[:, :W].contiguous(), base[:, 32:32 + W]):  # dense and pitched
             for chunk in ["0", "5", "32"]:
-                if chunk == "0":
-                    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
-                else:
-                    monkeypatch.setenv("DWT2D_CHUNK_ROWS", chunk)
-                monkeypatch.setenv("DWT2D_TMA", "0")
+                plan.tune(chunk_rows=int(chunk), tma=0)
                 a = plan.forward_level(img)
-                monkeypatch.setenv("DWT2D_TMA", "2")
+                plan.tune(tma=2)
                 b = plan.forward_level(img)
                 for j in range(4):
                     assert torch.equal(a[j], b[j]), (W, H, chunk, j)
-    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
     img = torch.from_numpy(O.random_image(1024, 768, 5)).to(cuda)
-    monkeypatch.setenv("DWT2D_TMA", "0")
+    plan.tune(chunk_rows=0, tma=0)
     a = plan.forward_mallat(img, 5)
-    monkeypatch.setenv("DWT2D_TMA", "2")
+    plan.tune(tma=2)
     b = plan.forward_mallat(img, 5)
     assert torch.equal(a, b)
 
@@ -254,21 +221,16 @@ def test_tma_staged_inverse_levels_bit_exact(dwt, cuda, w, monkeypatch):
     for W, H in [(64, 40), (256, 200), (2400, 96), (1024, 1024)]:
         planes = _to_dev(O.split(O.random_image(W, H, 21)), cuda)
         for chunk in ["0", "5", "32"]:
-            if chunk == "0":
-                monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
-            else:
-                monkeypatch.setenv("DWT2D_CHUNK_ROWS", chunk)
-            monkeypatch.setenv("DWT2D_TMA", "0")
+            inv.tune(chunk_rows=int(chunk), tma=0)
             a = inv.inverse_level(planes)
-            monkeypatch.setenv("DWT2D_TMA", "2")
+            inv.tune(tma=2)
             b = inv.inverse_level(planes)
             assert torch.equal(a, b), (W, H, chunk)
-    monkeypatch.delenv("DWT2D_CHUNK_ROWS", raising=False)
     coeffs = dwt.Plan(w, "nonseparable-lifting", optimized=True).forward_mallat(
         torch.from_numpy(O.random_image(1024, 768, 5)).to(cuda), 5)
-    monkeypatch.setenv("DWT2D_TMA", "0")
+    inv.tune(chunk_rows=0, tma=0)
     a = inv.inverse_mallat(coeffs, 5)
-    monkeypatch.setenv("DWT2D_TMA", "2")
+    inv.tune(tma=2)
     b = inv.inverse_mallat(coeffs, 5)
     assert torch.equal(a, b)
 
@@ -287,37 +249,16 @@ def test_level_pair_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     for W, H, L in [(1024, 768, 5), (256, 128, 3), (2400, 96, 2), (4096, 64, 2), (64, 64, 2)]:
         base = torch.from_numpy(O.random_image(W + 32, H, 13)).to(cuda)
         for img in (base[:, :W].contiguous(), base[:, 16:16 + W]):
-            monkeypatch.setenv("DWT2D_PAIR", "0")
+            plan.tune(pair=0)
             a = plan.forward_mallat(img, L)
-            monkeypatch.setenv("DWT2D_PAIR", "2")
-            for chunk in ["1", "3", "32"]:
-                monkeypatch.setenv("DWT2D_PAIR_CHUNK_ROWS", chunk)
+            plan.tune(pair=2)
+            for chunk in [1, 3, 32]:
+                plan.tune(pair_chunk_rows=chunk)
                 before = dwt.launch_count()
                 b = plan.forward_mallat(img, L)
                 torch.cuda.synchronize()
                 assert dwt.launch_count() - before == L - 1, (W, H, L)
                 assert torch.equal(a, b), (W, H, L, chunk)
-
-
-@pytest.mark.parametrize("first", [2, 3, 5])
-def test_deep_level_wavefront_bit_exact(dwt, cuda, first, monkeypatch):
-    """Levels 1..first-1 one launch each, levels first..L as one wavefront:
-    same bits as one launch per level, and first-1 + 1 launches."""
-    import torch
-    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
-    W, H, L = 2048, 1024, 7
-    img = torch.from_numpy(O.random_image(W, H, 3)).to(cuda)
-    monkeypatch.setenv("DWT2D_WAVEFRONT", "0")
-    a = plan.forward_mallat(img, L)
-    monkeypatch.delenv("DWT2D_WAVEFRONT")
-    monkeypatch.setenv("DWT2D_WAVE_FROM", str(first))
-    for cd in ["1", "2", "4", "7"]:
-        monkeypatch.setenv("DWT2D_WAVE_CHUNK_ROWS", cd)
-        before = dwt.launch_count()
-        b = plan.forward_mallat(img, L)
-        torch.cuda.synchronize()
-        assert dwt.launch_count() - before == first, cd
-        assert torch.equal(a, b), (first, cd)
 
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf97", "separable-lifting", False),
@@ -330,11 +271,10 @@ def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     planes = _to_dev(O.split(O.random_image(256, 200, 4)), cuda)
     img = torch.from_numpy(O.random_image(256, 200, 4)).to(cuda)
     for chunk in ["3", "7", "16", "1000"]:
-        monkeypatch.setenv("DWT2D_CHUNK_ROWS", chunk)
-        monkeypatch.setenv("DWT2D_ALTERNATE", "0")
+        plan.tune(chunk_rows=int(chunk), alternate=0)
         a = plan.run(planes)
         fa = plan.forward_level(img) if s != "inverse-lifting" else a
-        monkeypatch.setenv("DWT2D_ALTERNATE", "2")  # also on this single-wave level
+        plan.tune(alternate=2)  # also on this single-wave level
         b = plan.run(planes)
         fb = plan.forward_level(img) if s != "inverse-lifting" else b
         for j in range(4):
@@ -342,15 +282,16 @@ def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
             assert torch.equal(fa[j], fb[j]), (chunk, j)
 
 
-@pytest.mark.parametrize("band_rows", ["64", "96", "10000"])
+@pytest.mark.parametrize("band_rows", ["0", "64", "96", "10000"])
 def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, monkeypatch):
     """The pipelined host entry point (row bands uploaded while level 1 runs
     on earlier bands, halos from neighbouring bands) equals the device
     pyramid bit for bit, for several band splits incl. a ragged last band."""
     import torch
-    monkeypatch.setenv("DWT2D_HOST_BAND_ROWS", band_rows)
-    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
-    for W, H, L in [(256, 320, 3), (128, 96, 1)]:
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True).tune(host_band_rows=int(band_rows))
+    # H = 1026 / 1028: the default bands leave a 2-row remainder, which the
+    # last band absorbs (a 2-row band would be thinner than its halo)
+    for W, H, L in [(256, 320, 3), (128, 96, 1), (128, 1026, 1), (128, 1028, 2), (64, 4100, 2)]:
         img = O.random_image(W, H, 21)
         dev = plan.forward_mallat(torch.from_numpy(img).to(cuda), L).cpu().numpy()
         host = plan.forward_mallat_host(img, L)
@@ -397,11 +338,6 @@ def test_launch_count_and_native_library_loaded(dwt, cuda, monkeypatch):
     plan.forward_mallat(img, 8)  # level 8 is 1 component wide: no vector path, one launch per level
     torch.cuda.synchronize()
     assert dwt.launch_count() - before == 8
-    monkeypatch.setenv("DWT2D_WAVEFRONT", "1")
-    before = dwt.launch_count()
-    plan.forward_mallat(img, 6)  # wavefront: all levels in one launch
-    torch.cuda.synchronize()
-    assert dwt.launch_count() - before == 1
     maps = open("/proc/self/maps").read()
     assert str(native.LIB_PATH) in maps
 
@@ -464,8 +400,8 @@ def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, tiles
     forward level from the image, inverse level to the image, incl. odd
     (scalar-path) widths and grids just above the crop threshold."""
     import torch
-    monkeypatch.setenv("DWT2D_CROP_TILES", tiles)  # one tile launch, or one launch per sub-step
-    fused = dwt.Plan(w, s, optimized=opt, extension="symmetric")
+    # one tile launch, or one launch per sub-step
+    fused = dwt.Plan(w, s, optimized=opt, extension="symmetric").tune(crop_tiles=int(tiles))
     monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
     gen = dwt.Plan(w, s, optimized=opt, extension="symmetric")
     monkeypatch.delenv("DWT2D_FORCE_GENERIC")

@@ -96,6 +96,45 @@ def test_gloo_strip_pyramid_equals_full_image(world, wavelet, scheme, opt, pair)
     assert q.get(timeout=10) < 1e-12
 
 
+def _pitched_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        strip = torch.arange(60.0).reshape(10, 6) + 1000 * rank
+        # the C++ driver's halo rows from level 3 on: w floats of a wider pitch
+        buf = torch.full((8, 16), -1.0)
+        top, bottom = buf[:4, :6], buf[4:7, :6]
+        assert not top.is_contiguous()
+        S.HaloExchange()(strip, 4, 3, top=top, bottom=bottom)
+        prev, nxt = S.ring_neighbours(rank, world)
+        ok = (torch.equal(top, torch.arange(60.0).reshape(10, 6)[-4:] + 1000 * prev) and
+              torch.equal(bottom, torch.arange(60.0).reshape(10, 6)[:3] + 1000 * nxt) and
+              bool((buf[:, 6:] == -1).all()))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_exchange_into_pitched_views(world):
+    """HaloExchange with world > 1 fills non-contiguous (pitched) halo views
+    row by row and leaves the rest of the pitch alone."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pitched_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    assert all(ok for _, ok in res), res
+
+
 def test_exchange_into_given_buffers():
     """HaloExchange receives into caller buffers (the C++ strip driver's
     callback contract); single rank: periodic wrap."""
@@ -151,14 +190,13 @@ class VirtualRing:
 @pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
                                                 ("cdf97", "separable-convolution", False),
                                                 ("dd137", "nonseparable-lifting", True)])
-def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, tma, pair, monkeypatch):
+def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, tma, pair):
     """The halo-row path of the fused kernel reproduces the single-GPU
     pyramid bit for bit (same arithmetic; halo rows are the same data), with
     register prefetch (DWT2D_TMA=0), TMA-staged rows (=2), and with levels
     1+2 as one fused pass from 6*up/6*down halo rows (pair)."""
     import paper_1704_08657_b200 as dwt
-    monkeypatch.setenv("DWT2D_TMA", tma)
-    plan = dwt.Plan(wavelet, scheme, optimized=opt)
+    plan = dwt.Plan(wavelet, scheme, optimized=opt).tune(tma=int(tma))
     up, down = plan.info["reach_up"], plan.info["reach_down"]
     W, Hs, L = 256, 128, 4
     img = torch.from_numpy(O.random_image(W, Hs * world, 3)).to(cuda)
@@ -195,14 +233,13 @@ def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme
                                                 ("cdf53", "separable-lifting", False),
                                                 ("dd137", "nonseparable-lifting", True)])
 @pytest.mark.parametrize("pair", ["1", "0"])
-def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, pair, monkeypatch):
+def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, pair):
     """The C++ strip-pyramid driver (dwt2d_forward_mallat_strip) with a
     Python halo-exchange callback reproduces the single-GPU pyramid bit for
     bit: world 1 without a callback (periodic wrap inside the strip), 2 and
     4 virtual ranks as threads; with and without the fused level pair."""
     import paper_1704_08657_b200 as dwt
-    monkeypatch.setenv("DWT2D_PAIR", pair)
-    plan = dwt.Plan(wavelet, scheme, optimized=opt)
+    plan = dwt.Plan(wavelet, scheme, optimized=opt).tune(pair=int(pair))
     W, Hs, L = 256, 128, 4
     img = torch.from_numpy(O.random_image(W, Hs * world, 3)).to(cuda)
     full = plan.forward_mallat(img, L)
