@@ -217,6 +217,48 @@ DWT2D_B200_API int dwt2d_forward_mallat_strip(const dwt2d_plan* plan, const floa
                                               size_t out_pitch, void* scratch, dwt2d_halo_fn exchange,
                                               void* user, void* stream);
 
+/* --- sharded pyramid: row strips over GPUs, device-side halo exchange -----
+ * The in-library multi-GPU driver (SURVEY §8(b) dwt_forward_sharded, §8(e);
+ * reference analogue: row bands + one barrier per step, executor.hpp:211-225).
+ * A periodic W x (world * strip_height) image is split into `world` row
+ * strips in a ring; rank r holds rows [r * strip_height, (r+1) * strip_height).
+ * Per level every rank pushes its boundary rows into its ring neighbours'
+ * exchange windows over peer memory (NVLink) and signals a counter there,
+ * runs the level's interior rows, waits for its own counters and finishes
+ * the border rows — all on the device, in stream order, graph-capturable.
+ * Output per rank: its strip-Mallat buffer (the strip's rows of every band
+ * in the Mallat layout of the strip). strip_height must be divisible by
+ * 2^levels and every level's strip at least as tall as its halo rows.
+ *
+ * One shard per rank: create on the rank's device (current device), connect
+ * to the ring neighbours — same process: dwt2d_shard_connect (enables peer
+ * access); other processes: exchange dwt2d_shard_export handles (64 bytes,
+ * CUDA IPC) and dwt2d_shard_connect_ipc — then call
+ * dwt2d_shard_forward_mallat per pyramid on every rank. world == 1 needs no
+ * connect (the ring of one wraps onto itself). A ring that stops making
+ * progress traps after 20 s (dwt2d_shard_status reads the error word: 1 =
+ * neighbour never finished a pyramid, 2 = halo never arrived). */
+typedef struct dwt2d_shard dwt2d_shard;
+#define DWT2D_SHARD_HANDLE_BYTES 64
+DWT2D_B200_API int dwt2d_shard_create(const dwt2d_plan* plan, int width, int strip_height, int levels,
+                                      int rank, int world, dwt2d_shard** shard);
+DWT2D_B200_API void dwt2d_shard_destroy(dwt2d_shard* shard);
+DWT2D_B200_API int dwt2d_shard_export(const dwt2d_shard* shard, void* handle, size_t len);
+DWT2D_B200_API int dwt2d_shard_connect(dwt2d_shard* shard, const dwt2d_shard* prev, const dwt2d_shard* next);
+DWT2D_B200_API int dwt2d_shard_connect_ipc(dwt2d_shard* shard, const void* prev_handle,
+                                           const void* next_handle);
+DWT2D_B200_API int dwt2d_shard_forward_mallat(dwt2d_shard* shard, const float* strip, size_t pitch,
+                                              float* out, size_t out_pitch, void* stream);
+DWT2D_B200_API int dwt2d_shard_status(const dwt2d_shard* shard, int* error);
+/* Single-process driver over `nranks` ranks on `devices` (a device may
+ * repeat: virtual ranks on one GPU): strips[r] / out[r] live on devices[r];
+ * streams[r] (or NULL: each device's default stream). The shards are cached
+ * in the plan per geometry. Enqueues every rank's work and returns. */
+DWT2D_B200_API int dwt2d_forward_mallat_sharded(const dwt2d_plan* plan, int nranks, const int* devices,
+                                                const float* const* strips, const size_t* pitch, int width,
+                                                int strip_height, int levels, float* const* out,
+                                                const size_t* out_pitch, void* const* streams);
+
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by
  * LL | HL over LH | HH (each w/2 x h/2). `scratch` holds intermediate LL

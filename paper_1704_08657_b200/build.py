@@ -101,6 +101,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     for s in RUNTIME_SRCS:
         units.append(("cxx", CSRC / s))
     units.append(("nvcc", CSRC / "kernels/generic_step.cu"))
+    units.append(("nvcc", CSRC / "kernels/exchange.cu"))
     for cu in sorted((CSRC / "generated").glob("*.cu")):
         units.append(("nvcc", cu))
     objs = []

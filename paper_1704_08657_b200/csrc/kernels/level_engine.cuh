@@ -685,8 +685,8 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   const int lane = threadIdx.x & 31;
   const int strip = wid % a.nstrips;
   const int xc = (strip * kOutLanes - 1 + lane) * CW;  // first component column of this lane
-  const int y0 = chunk * a.chunk_rows;
-  const int y1 = min(a.h2, y0 + a.chunk_rows);
+  const int y0 = a.y_begin + chunk * a.chunk_rows;
+  const int y1 = min(a.y_end > 0 ? a.y_end : a.h2, y0 + a.chunk_rows);
   // first input row streamed, and the output row of iteration 0
   const int n0 = UPW ? y1 - 1 + M::L : y0 - M::U;
   const int yfirst = UPW ? n0 + M::U : n0 - M::L;

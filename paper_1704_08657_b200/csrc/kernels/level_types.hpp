@@ -33,8 +33,9 @@ struct LevelArgs {
   long long out_pitch[4];
   int w2, h2;           // component grid size
   int nstrips;          // ceil(w2 / (30 * CW))
-  int nchunks;          // ceil(h2 / chunk_rows)
+  int nchunks;          // ceil((y_end - y_begin) / chunk_rows)
   int chunk_rows;
+  int y_begin, y_end;   // output component rows covered by the chunks (y_end 0: h2)
   int vec;              // 1: vector fast path valid (w2 % CW == 0, 16 B aligned)
   int reverse;          // 1: hand out chunks bottom-up (see capi.cpp forward_mallat)
   int alternate;        // 1: odd chunks stream bottom-up (shared warm-up rows hit L2)
@@ -61,6 +62,7 @@ constexpr int kPairLanes = 28;  // lanes 2..29 store both levels
 struct PairArgs {
   LevelArgs l1, l2;
   int nstrips, chunk_rows, nchunks;
+  int m_begin, m_end;   // level-2 output rows covered by the chunks (m_end 0: l2.h2)
 };
 using PairLaunch = cudaError_t (*)(const PairArgs&, cudaStream_t);
 
@@ -129,6 +131,33 @@ cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, bool pdl, 
 // grids) in one launch
 constexpr int kMaxGenericRegions = 4;
 cudaError_t launch_generic_step(const GenericStepArgs* a, int n, bool pdl, cudaStream_t st);
+
+// Halo exchange of a row-strip sharded pyramid over peer memory
+// (kernels/exchange.cu). Pointers named prev/next live in the ring
+// neighbours' exchange windows (peer-mapped), the rest in this rank's.
+struct HaloPushArgs {
+  const float* src;      // the level input strip (height x width, src_pitch)
+  long long src_pitch;
+  int width, height;
+  int rows_first;        // src rows [0, rows_first) -> dst_prev (prev's bottom halo)
+  int rows_last;         // src rows [height - rows_last, height) -> dst_next (next's top halo)
+  float* dst_prev;
+  float* dst_next;
+  long long dst_pitch;
+  int vec;               // width, pitches and pointers allow float4 copies
+  unsigned* flag_prev;   // prev's bottom-halo arrival counter
+  unsigned* flag_next;   // next's top-halo arrival counter
+  unsigned* arrive;      // this rank's CTA arrival counter (last CTA signals)
+  int first_step;        // first push of a pyramid: wait for *done >= 2 * *pyramids
+  const unsigned* done;
+  const unsigned* pyramids;
+  unsigned* error;
+  unsigned long long timeout_ns;
+};
+cudaError_t launch_halo_push(const HaloPushArgs& a, int sms, cudaStream_t st);
+cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag, unsigned* seen, unsigned* error,
+                             unsigned long long timeout_ns, cudaStream_t st);
+cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsigned* pyramids, cudaStream_t st);
 
 const std::vector<PlanEntry>& plan_registry();
 const PlanEntry* find_plan(unsigned long long fingerprint);

@@ -47,7 +47,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
   const int lane = threadIdx.x & 31;
   const int xc1 = (strip * kPairLanes - 2 + lane) * CW1;  // level-1 component column of this lane
   const int xc2 = xc1 / 2;                                // exact: xc1 is a multiple of 4
-  const int m0 = chunk * t.chunk_rows, m1 = min(a2.h2, m0 + t.chunk_rows);
+  const int m0 = t.m_begin + chunk * t.chunk_rows, m1 = min(t.m_end > 0 ? t.m_end : a2.h2, m0 + t.chunk_rows);
   const int n02 = m0 - U;              // first level-2 input row
   const int rows2 = (m1 - m0) + U + L;
   const int n01 = 2 * n02 - U;         // first level-1 input row

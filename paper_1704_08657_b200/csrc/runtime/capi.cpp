@@ -90,13 +90,26 @@ struct dwt2d_plan {
   };
   mutable std::mutex dev_mu;
   mutable DeviceTables dev[kMaxDevices];
-  ~dwt2d_plan() {
+  // rings of shards of dwt2d_forward_mallat_sharded, one per geometry
+  struct ShardRing {
+    std::vector<long long> key;
+    std::vector<dwt2d_shard*> shards;
+  };
+  mutable std::mutex shard_mu;
+  mutable std::vector<ShardRing> shard_cache;
+  ~dwt2d_plan();
+  void free_device_tables() {
     for (DeviceTables& d : dev) {
       if (d.taps) cudaFree(d.taps);
       if (d.rows) cudaFree(d.rows);
     }
   }
 };
+
+// One rank's share of a row-strip sharded forward pyramid:
+// the exchange window its ring neighbours write halo rows into, the LL
+// workspace, and the neighbours' windows once connected. Defined below.
+struct dwt2d_shard;
 
 namespace {
 
@@ -201,7 +214,12 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
-  a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, a.h2) : chunk_rows_for(p, a.h2, a.nstrips);
+  // output rows covered by this launch: [y_begin, y_end) (a strip level's
+  // interior or border rows), by default the whole level
+  if (a.y_end <= 0) a.y_end = a.h2;
+  if (a.y_begin < 0 || a.y_begin >= a.y_end || a.y_end > a.h2) fail(DWT2D_EINVAL, "level row range");
+  const int span = a.y_end - a.y_begin;
+  a.chunk_rows = chunk_override > 0 ? std::min(chunk_override, span) : chunk_rows_for(p, span, a.nstrips);
   // TMA-staged input rows (level_engine.cuh: TmaRowReader) for forward levels
   // of CW-4 programs (PlanEntry::stage_ok) that stream at least 512 MiB from
   // HBM: level 1 of 16384^2 346 vs 355 us, with ~10 waves of 32-row chunks
@@ -219,11 +237,11 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
                ((bytes >= (size_t(512) << 20) && e.stage_ok) || force) ? 1 : 0;
     if (a.staged && chunk_override <= 0 && p.tune.chunk_rows <= 0) {
       const long long resident = resident_warps(p);
-      const long long rows_total = (long long)a.h2 * a.nstrips;
-      a.chunk_rows = int(std::max<long long>(8, std::min<long long>(a.h2, (rows_total + 10 * resident - 1) / (10 * resident))));
+      const long long rows_total = (long long)span * a.nstrips;
+      a.chunk_rows = int(std::min<long long>(span, std::max<long long>(8, (rows_total + 10 * resident - 1) / (10 * resident))));
     }
   }
-  a.nchunks = (a.h2 + a.chunk_rows - 1) / a.chunk_rows;
+  a.nchunks = (span + a.chunk_rows - 1) / a.chunk_rows;
   // bottom-up odd chunks pay once the level streams from HBM (their shared
   // warm-up rows then meet in L2: 4096^2 single level 30.7 vs 32.8 us); a
   // level whose input (16 B per quad) fits comfortably in L2 streams
@@ -654,11 +672,14 @@ void run_pair(const dwt2d_plan& p, gpu::PairArgs& t, cudaStream_t st) {
   }
   const long long resident = (long long)std::max(1, per_sm) * gpu::kWarpsPerCta * sm_count();
   const long long per_wave = std::max<long long>(1, resident / t.nstrips);  // chunks per full wave
-  const long long waves = std::max<long long>(1, (t.l2.h2 + 128 * per_wave) / (256 * per_wave));
-  long long chunk = (t.l2.h2 + waves * per_wave - 1) / (waves * per_wave);
+  if (t.m_end <= 0) t.m_end = t.l2.h2;
+  if (t.m_begin < 0 || t.m_begin >= t.m_end || t.m_end > t.l2.h2) fail(DWT2D_EINVAL, "level pair row range");
+  const int span = t.m_end - t.m_begin;
+  const long long waves = std::max<long long>(1, (span + 128 * per_wave) / (256 * per_wave));
+  long long chunk = (span + waves * per_wave - 1) / (waves * per_wave);
   if (p.tune.pair_chunk_rows > 0) chunk = p.tune.pair_chunk_rows;
-  t.chunk_rows = int(std::min<long long>(chunk, t.l2.h2));
-  t.nchunks = (t.l2.h2 + t.chunk_rows - 1) / t.chunk_rows;
+  t.chunk_rows = int(std::min<long long>(chunk, span));
+  t.nchunks = (span + t.chunk_rows - 1) / t.chunk_rows;
   cuda_check(p.entry->pair(t, st), "level pair kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -821,6 +842,253 @@ void forward_mallat_strip(const dwt2d_plan& p, const float* strip, size_t pitch,
     launch(p, a, kFromImage, st);
     cur = ll, cur_pitch = llp;
   }
+}
+
+// ------------------------------------------ sharded pyramid (multi-GPU)
+//
+// Row strips of one periodic image, one per rank (GPU), in a ring. Each
+// level (or the fused level pair) needs the 2*up (6*up for the pair) image
+// rows above the strip from the previous rank and 2*down (6*down) below it
+// from the next rank. The exchange runs on the device (kernels/exchange.cu):
+// every rank pushes its boundary rows straight into the neighbours'
+// exchange windows over NVLink (peer stores) and signals a counter there;
+// the level then runs on its interior rows — which need no halo — while
+// the neighbours' rows arrive, waits for its own counters, and finishes the
+// border rows. No host round trip per level; the whole strip pyramid is
+// stream-ordered and graph-capturable. World 1 is the same ring with a
+// single member: the pushes wrap the strip onto itself (periodic image).
+
+// window header: counters on separate 128-byte lines (unsigned words)
+constexpr int kTopArrivals = 0, kBotArrivals = 32, kDone = 64, kSeen = 96, kArrive = 128, kPyramids = 160,
+              kError = 192;
+constexpr size_t kHeaderBytes = 1024;
+constexpr unsigned long long kExchangeTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s: a broken ring traps
+
+struct ExchangeStep {
+  int level;             // first level of the step (1-based)
+  bool pair;             // levels `level` and `level` + 1 in one pass
+  int width, height;     // the step's input strip (image rows)
+  int trows, brows;      // halo image rows above / below
+  size_t top_off, bot_off;  // bytes into the window
+  size_t pitch;          // halo pitch (floats)
+};
+
+}  // namespace
+
+struct dwt2d_shard {
+  const dwt2d_plan* plan = nullptr;
+  int device = 0, rank = 0, world = 1, W = 0, H = 0, levels = 0;
+  std::vector<ExchangeStep> steps;
+  char* window = nullptr;
+  size_t window_bytes = 0;
+  float* ws = nullptr;  // LL bands of levels 1 .. levels-1
+  const dwt2d_shard* prev = nullptr;
+  const dwt2d_shard* next = nullptr;
+  char* prev_win = nullptr;  // neighbours' windows (peer pointers)
+  char* next_win = nullptr;
+  char* ipc_open[2] = {nullptr, nullptr};  // handles opened with cudaIpcOpenMemHandle
+  bool connected = false;
+  unsigned* word(char* win, int w) const { return reinterpret_cast<unsigned*>(win) + w; }
+  ~dwt2d_shard() {
+    int cur = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess) cur = device;
+    cudaSetDevice(device);
+    for (char* p : ipc_open)
+      if (p) cudaIpcCloseMemHandle(p);
+    if (window) cudaFree(window);
+    if (ws) cudaFree(ws);
+    cudaSetDevice(cur);
+    cudaGetLastError();
+  }
+};
+
+dwt2d_plan::~dwt2d_plan() {
+  for (ShardRing& r : shard_cache)
+    for (dwt2d_shard* s : r.shards) delete s;
+  free_device_tables();
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cuda_check(cudaGetDevice(&prev), "current device");
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "set device");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+bool shard_pair(const dwt2d_plan& p, int W, int H, int levels) {
+  return levels >= 2 && pair_capable(p) && p.tune.pair != 0 && W % 16 == 0 && H % 4 == 0;
+}
+
+// exchange steps and window layout of a strip pyramid
+void plan_steps(dwt2d_shard& s) {
+  const dwt2d_plan& p = *s.plan;
+  size_t off = kHeaderBytes;
+  auto add = [&](int level, bool pair, int w, int h, int tr, int br) {
+    if (h < tr || h < br)
+      fail(DWT2D_EUNSUPPORTED, "sharded pyramid: the strip of level " + std::to_string(level) + " (" +
+                                   std::to_string(h) + " rows) is thinner than its halo; use fewer ranks or levels");
+    ExchangeStep e{level, pair, w, h, tr, br, 0, 0, ws_align(size_t(w))};
+    e.top_off = off, off += ((size_t(tr) * e.pitch * 4 + 255) & ~size_t(255));
+    e.bot_off = off, off += ((size_t(br) * e.pitch * 4 + 255) & ~size_t(255));
+    s.steps.push_back(e);
+  };
+  int l = 1;
+  if (shard_pair(p, s.W, s.H, s.levels)) {
+    add(1, true, s.W, s.H, 6 * p.up, 6 * p.down);
+    l = 3;
+  }
+  for (; l <= s.levels; ++l) add(l, false, s.W >> (l - 1), s.H >> (l - 1), 2 * p.up, 2 * p.down);
+  s.window_bytes = off;
+}
+
+float* step_top(const dwt2d_shard& s, const ExchangeStep& e) { return reinterpret_cast<float*>(s.window + e.top_off); }
+float* step_bot(const dwt2d_shard& s, const ExchangeStep& e) { return reinterpret_cast<float*>(s.window + e.bot_off); }
+
+void shard_connect_windows(dwt2d_shard& s, char* prev_win, char* next_win) {
+  s.prev_win = prev_win, s.next_win = next_win;
+  s.connected = true;
+}
+
+// input rows of step e (the strip, or the LL band the previous step wrote)
+struct StepIO {
+  const float* cur;
+  size_t cur_pitch;
+};
+StepIO step_input(const dwt2d_shard& s, size_t e, const float* strip, size_t pitch, float* out, size_t op) {
+  if (e == 0) return {strip, pitch};
+  const ExchangeStep& prev = s.steps[e - 1];
+  const int l = prev.pair ? prev.level + 1 : prev.level;  // last level the previous step computed
+  // that level's LL: a workspace slot (never the output: step e exists, so l < levels)
+  (void)out, (void)op;
+  return {ll_slot(s.ws, s.W, s.H, l), size_t(s.W >> l)};
+}
+
+void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, cudaStream_t st) {
+  const ExchangeStep& x = s.steps[e];
+  gpu::HaloPushArgs a{};
+  a.src = io.cur, a.src_pitch = (long long)io.cur_pitch;
+  a.width = x.width, a.height = x.height;
+  a.rows_first = x.brows, a.rows_last = x.trows;  // my first rows are prev's bottom halo
+  a.dst_prev = reinterpret_cast<float*>(s.prev_win + x.bot_off);
+  a.dst_next = reinterpret_cast<float*>(s.next_win + x.top_off);
+  a.dst_pitch = (long long)x.pitch;
+  a.vec = (x.width % 4 == 0 && io.cur_pitch % 4 == 0 && aligned(io.cur, 16)) ? 1 : 0;
+  a.flag_prev = s.word(s.prev_win, kBotArrivals);
+  a.flag_next = s.word(s.next_win, kTopArrivals);
+  a.arrive = s.word(s.window, kArrive);
+  a.first_step = e == 0 ? 1 : 0;
+  a.done = s.word(s.window, kDone);
+  a.pyramids = s.word(s.window, kPyramids);
+  a.error = s.word(s.window, kError);
+  a.timeout_ns = kExchangeTimeoutNs;
+  cuda_check(gpu::launch_halo_push(a, sm_count(), st), "halo push launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void shard_wait(dwt2d_shard& s, cudaStream_t st) {
+  cuda_check(gpu::launch_halo_wait(s.word(s.window, kTopArrivals), s.word(s.window, kBotArrivals),
+                                   s.word(s.window, kSeen), s.word(s.window, kError), kExchangeTimeoutNs, st),
+             "halo wait launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void shard_done(dwt2d_shard& s, cudaStream_t st) {
+  cuda_check(gpu::launch_pyramid_done(s.word(s.prev_win, kDone), s.word(s.next_win, kDone),
+                                      s.word(s.window, kPyramids), st),
+             "pyramid done launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+// Output rows of step e that need no halo: the interior [lo, hi) of the
+// step's (level-2 for the pair) output rows, or lo == hi when the interior
+// is too short to be worth its own launch.
+void step_interior(const dwt2d_shard& s, const ExchangeStep& x, int& lo, int& hi, int& rows) {
+  const dwt2d_plan& p = *s.plan;
+  if (x.pair) {
+    // level-2 rows [m0, m1) read level-1 component rows [2 m0 - 3U, 2 m1 + 3L)
+    rows = x.height / 4;
+    lo = (3 * p.up + 1) / 2;
+    hi = (x.height / 2 - 3 * p.down) / 2;
+  } else {
+    rows = x.height / 2;
+    lo = p.up;
+    hi = rows - p.down;
+  }
+  if (hi - lo < 16) lo = hi = 0;
+}
+
+// part: 0 interior rows, 1 border rows (all rows when there is no interior)
+void shard_compute(dwt2d_shard& s, size_t e, const StepIO& io, float* out, size_t op, int part, cudaStream_t st) {
+  const dwt2d_plan& p = *s.plan;
+  const ExchangeStep& x = s.steps[e];
+  int lo, hi, rows;
+  step_interior(s, x, lo, hi, rows);
+  std::vector<std::pair<int, int>> ranges;
+  if (part == 0) {
+    if (hi > lo) ranges.push_back({lo, hi});
+  } else if (hi > lo) {
+    if (lo > 0) ranges.push_back({0, lo});
+    if (hi < rows) ranges.push_back({hi, rows});
+  } else {
+    ranges.push_back({0, rows});
+  }
+  if (ranges.empty()) return;
+  const float* top = step_top(s, x);
+  const float* bottom = step_bot(s, x);
+  const int W = x.width, H = x.height;
+  const bool last = (x.pair ? x.level + 1 : x.level) == s.levels;
+  if (x.pair) {
+    const int w2 = W / 2, h2 = H / 2, w4 = W / 4, h4 = H / 4;
+    float* const d1[3] = {out + w2, out + size_t(h2) * op, out + size_t(h2) * op + w2};
+    float* ll2 = last ? out : ll_slot(s.ws, s.W, s.H, 2);
+    const size_t ll2p = last ? op : size_t(w4);
+    float* const d2[4] = {ll2, out + w4, out + size_t(h4) * op, out + size_t(h4) * op + w4};
+    for (const auto& r : ranges) {
+      gpu::PairArgs t{};
+      gpu::LevelArgs& a = t.l1;
+      for (int j = 0; j < 4; ++j) {
+        a.in[j] = io.cur, a.in_pitch[j] = (long long)io.cur_pitch;
+        a.halo_top[j] = top, a.halo_bot[j] = bottom;
+        a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)x.pitch;
+        a.out[j] = d1[j == 0 ? 0 : j - 1], a.out_pitch[j] = (long long)op;
+        t.l2.in[j] = io.cur, t.l2.in_pitch[j] = (long long)io.cur_pitch;
+        t.l2.out[j] = d2[j], t.l2.out_pitch[j] = (long long)(j == 0 ? ll2p : op);
+      }
+      a.halo = 1, a.up = 3 * p.up, a.down = 3 * p.down;
+      a.w2 = w2, a.h2 = h2;
+      t.l2.w2 = w4, t.l2.h2 = h4;
+      prepare(p, t.l1, kFromImage);
+      prepare(p, t.l2, kFromImage);
+      if (!t.l1.vec || !t.l2.vec)
+        fail(DWT2D_EINVAL, "sharded pyramid: strips and outputs need 16-byte aligned rows (pitches multiple of 4)");
+      t.m_begin = r.first, t.m_end = r.second;
+      run_pair(p, t, st);
+    }
+    return;
+  }
+  const int w2 = W / 2, h2 = H / 2;
+  float* ll = last ? out : ll_slot(s.ws, s.W, s.H, x.level);
+  const size_t llp = last ? op : size_t(w2);
+  for (const auto& r : ranges) {
+    gpu::LevelArgs a{};
+    fill_forward_level(a, io.cur, io.cur_pitch, ll, llp, out, op, w2, h2);
+    for (int j = 0; j < 4; ++j) {
+      a.halo_top[j] = top, a.halo_bot[j] = bottom;
+      a.halo_top_pitch[j] = a.halo_bot_pitch[j] = (long long)x.pitch;
+    }
+    a.halo = 1, a.up = p.up, a.down = p.down;
+    a.y_begin = r.first, a.y_end = r.second;
+    launch(p, a, kFromImage, st);
+  }
+}
+
+void check_shard_args(const dwt2d_shard& s, const float* strip, const float* out) {
+  if (!strip || !out) fail(DWT2D_EINVAL, "null argument");
+  if (!s.connected) fail(DWT2D_EINVAL, "sharded pyramid: shard is not connected to its ring neighbours");
 }
 
 // ------------------------------------------------- host end-to-end pipeline
@@ -1404,6 +1672,197 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
     for (int j = 0; j < 4; ++j)
       cuda_check(cudaMemcpyAsync(out[j], dout[j], n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
     cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
+  });
+}
+
+// ------------------------------------------------ sharded pyramid (C ABI)
+
+int dwt2d_shard_create(const dwt2d_plan* p, int width, int strip_height, int levels, int rank, int world,
+                       dwt2d_shard** out) {
+  return guard([&] {
+    require_plan(p);
+    if (!out) fail(DWT2D_EINVAL, "null argument");
+    *out = nullptr;
+    if (!p->forward) fail(DWT2D_EINVAL, "shard: plan is an inverse plan");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (!p->entry || p->extension != DWT2D_PERIODIC)
+      fail(DWT2D_EUNSUPPORTED, "sharded pyramid: needs a fused kernel and periodic extension");
+    if (world < 1 || rank < 0 || rank >= world) fail(DWT2D_EINVAL, "shard: rank outside [0, world)");
+    check_pyramid(width, strip_height, levels);
+    auto sh = std::make_unique<dwt2d_shard>();
+    sh->plan = p;
+    sh->device = current_device();
+    sh->rank = rank, sh->world = world, sh->W = width, sh->H = strip_height, sh->levels = levels;
+    plan_steps(*sh);
+    void* win = nullptr;
+    cuda_check(cudaMalloc(&win, sh->window_bytes), "exchange window allocation");
+    sh->window = static_cast<char*>(win);
+    cuda_check(cudaMemset(sh->window, 0, kHeaderBytes), "exchange window init");
+    const size_t ws = ll_offset(width, strip_height, levels) * sizeof(float);
+    if (ws) {
+      void* w = nullptr;
+      cuda_check(cudaMalloc(&w, ws), "shard workspace allocation");
+      sh->ws = static_cast<float*>(w);
+    }
+    cuda_check(cudaDeviceSynchronize(), "exchange window init");
+    if (world == 1) {  // the ring of one: pushes wrap the strip onto itself
+      sh->prev = sh->next = sh.get();
+      shard_connect_windows(*sh, sh->window, sh->window);
+    }
+    *out = sh.release();
+  });
+}
+
+void dwt2d_shard_destroy(dwt2d_shard* s) { delete s; }
+
+int dwt2d_shard_export(const dwt2d_shard* s, void* handle, size_t len) {
+  return guard([&] {
+    if (!s || !handle) fail(DWT2D_EINVAL, "null argument");
+    if (len < sizeof(cudaIpcMemHandle_t)) fail(DWT2D_EINVAL, "shard_export: handle buffer too small");
+    DeviceGuard g(s->device);
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, s->window), "IPC handle of the exchange window");
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int dwt2d_shard_connect(dwt2d_shard* s, const dwt2d_shard* prev, const dwt2d_shard* next) {
+  return guard([&] {
+    if (!s || !prev || !next) fail(DWT2D_EINVAL, "null argument");
+    for (const dwt2d_shard* n : {prev, next})
+      if (n->W != s->W || n->H != s->H || n->levels != s->levels || n->steps.size() != s->steps.size() ||
+          n->window_bytes != s->window_bytes)
+        fail(DWT2D_EINVAL, "shard_connect: neighbours must share width, strip height, levels and plan geometry");
+    DeviceGuard g(s->device);
+    for (const dwt2d_shard* n : {prev, next})
+      if (n->device != s->device) {
+        int can = 0;
+        cuda_check(cudaDeviceCanAccessPeer(&can, s->device, n->device), "peer access query");
+        if (!can) fail(DWT2D_EUNSUPPORTED, "shard_connect: no peer access between the devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(n->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "enable peer access");
+        cudaGetLastError();
+      }
+    s->prev = prev, s->next = next;
+    shard_connect_windows(*s, prev->window, next->window);
+  });
+}
+
+int dwt2d_shard_connect_ipc(dwt2d_shard* s, const void* prev_handle, const void* next_handle) {
+  return guard([&] {
+    if (!s || !prev_handle || !next_handle) fail(DWT2D_EINVAL, "null argument");
+    DeviceGuard g(s->device);
+    cudaIpcMemHandle_t hp, hn;
+    std::memcpy(&hp, prev_handle, sizeof hp);
+    std::memcpy(&hn, next_handle, sizeof hn);
+    void* pp = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&pp, hp, cudaIpcMemLazyEnablePeerAccess), "open the previous rank's window");
+    s->ipc_open[0] = static_cast<char*>(pp);
+    void* pn = pp;
+    if (std::memcmp(&hp, &hn, sizeof hp) != 0) {  // two ranks: prev == next, opened once
+      cuda_check(cudaIpcOpenMemHandle(&pn, hn, cudaIpcMemLazyEnablePeerAccess), "open the next rank's window");
+      s->ipc_open[1] = static_cast<char*>(pn);
+    }
+    s->prev = s->next = nullptr;
+    shard_connect_windows(*s, static_cast<char*>(pp), static_cast<char*>(pn));
+  });
+}
+
+int dwt2d_shard_forward_mallat(dwt2d_shard* s, const float* strip, size_t pitch, float* out, size_t out_pitch,
+                               void* stream) {
+  return guard([&] {
+    if (!s) fail(DWT2D_EINVAL, "null argument");
+    check_shard_args(*s, strip, out);
+    DeviceGuard g(s->device);
+    const cudaStream_t st = as_stream(stream);
+    for (size_t e = 0; e < s->steps.size(); ++e) {
+      const StepIO io = step_input(*s, e, strip, pitch, out, out_pitch);
+      shard_push(*s, e, io, st);
+      shard_compute(*s, e, io, out, out_pitch, 0, st);
+      shard_wait(*s, st);
+      shard_compute(*s, e, io, out, out_pitch, 1, st);
+    }
+    shard_done(*s, st);
+  });
+}
+
+int dwt2d_shard_status(const dwt2d_shard* s, int* error) {
+  return guard([&] {
+    if (!s || !error) fail(DWT2D_EINVAL, "null argument");
+    DeviceGuard g(s->device);
+    unsigned v = 0;
+    cuda_check(cudaMemcpy(&v, reinterpret_cast<const unsigned*>(s->window) + kError, sizeof v,
+                          cudaMemcpyDeviceToHost),
+               "read exchange status");
+    *error = int(v);
+  });
+}
+
+int dwt2d_forward_mallat_sharded(const dwt2d_plan* p, int nranks, const int* devices, const float* const* strips,
+                                 const size_t* pitch, int width, int strip_height, int levels, float* const* out,
+                                 const size_t* out_pitch, void* const* streams) {
+  return guard([&] {
+    require_plan(p);
+    if (nranks < 1 || !devices || !strips || !pitch || !out || !out_pitch) fail(DWT2D_EINVAL, "null argument");
+    // shards of this ring geometry, created and connected on first use
+    std::vector<long long> key{nranks, width, strip_height, levels};
+    for (int r = 0; r < nranks; ++r) key.push_back(devices[r]);
+    std::vector<dwt2d_shard*>* ring = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(p->shard_mu);
+      for (auto& c : p->shard_cache)
+        if (c.key == key) ring = &c.shards;
+      if (!ring) {
+        dwt2d_plan::ShardRing sr;
+        sr.key = key;
+        for (int r = 0; r < nranks; ++r) {
+          DeviceGuard g(devices[r]);
+          dwt2d_shard* sh = nullptr;
+          const int rc = dwt2d_shard_create(p, width, strip_height, levels, r, nranks, &sh);
+          if (rc != DWT2D_OK) {
+            for (dwt2d_shard* o : sr.shards) delete o;
+            fail(rc, g_error);
+          }
+          sr.shards.push_back(sh);
+        }
+        for (int r = 0; r < nranks && nranks > 1; ++r) {
+          const int rc = dwt2d_shard_connect(sr.shards[r], sr.shards[(r + nranks - 1) % nranks],
+                                             sr.shards[(r + 1) % nranks]);
+          if (rc != DWT2D_OK) {
+            for (dwt2d_shard* o : sr.shards) delete o;
+            fail(rc, g_error);
+          }
+        }
+        p->shard_cache.push_back(std::move(sr));
+        ring = &p->shard_cache.back().shards;
+      }
+    }
+    std::vector<dwt2d_shard*>& sh = *ring;
+    for (int r = 0; r < nranks; ++r) check_shard_args(*sh[r], strips[r], out[r]);
+    auto st = [&](int r) { return streams ? as_stream(streams[r]) : cudaStream_t(nullptr); };
+    // phase-major enqueue: every rank's push of a step before any rank's
+    // wait, so ranks sharing a device (or a stream) cannot block each other
+    for (size_t e = 0; e < sh[0]->steps.size(); ++e) {
+      std::vector<StepIO> io;
+      for (int r = 0; r < nranks; ++r) io.push_back(step_input(*sh[r], e, strips[r], pitch[r], out[r], out_pitch[r]));
+      for (int r = 0; r < nranks; ++r) {
+        DeviceGuard g(sh[r]->device);
+        shard_push(*sh[r], e, io[r], st(r));
+      }
+      for (int r = 0; r < nranks; ++r) {
+        DeviceGuard g(sh[r]->device);
+        shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], 0, st(r));
+      }
+      for (int r = 0; r < nranks; ++r) {
+        DeviceGuard g(sh[r]->device);
+        shard_wait(*sh[r], st(r));
+        shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], 1, st(r));
+      }
+    }
+    for (int r = 0; r < nranks; ++r) {
+      DeviceGuard g(sh[r]->device);
+      shard_done(*sh[r], st(r));
+    }
   });
 }
 

@@ -20,6 +20,7 @@ if not LIB_PATH.exists():
 lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL)
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = range(5)
+SHARD_HANDLE_BYTES = 64
 
 SCHEMES = {
     "separable-convolution": 0,
@@ -101,6 +102,18 @@ _SIGS = {
                                                 _P4, _S4, _p]),
     "dwt2d_inverse_level_strip": (ctypes.c_int, [_p, _P4, _S4, _P4, _P4, _S4, _p, _sz, ctypes.c_int,
                                                  ctypes.c_int, _p]),
+    "dwt2d_shard_create": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(_p)]),
+    "dwt2d_shard_destroy": (None, [_p]),
+    "dwt2d_shard_export": (ctypes.c_int, [_p, ctypes.c_char_p, _sz]),
+    "dwt2d_shard_connect": (ctypes.c_int, [_p, _p, _p]),
+    "dwt2d_shard_connect_ipc": (ctypes.c_int, [_p, ctypes.c_char_p, ctypes.c_char_p]),
+    "dwt2d_shard_forward_mallat": (ctypes.c_int, [_p, _p, _sz, _p, _sz, _p]),
+    "dwt2d_shard_status": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int)]),
+    "dwt2d_forward_mallat_sharded": (ctypes.c_int, [_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                                    ctypes.POINTER(_p), ctypes.POINTER(_sz), ctypes.c_int,
+                                                    ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p),
+                                                    ctypes.POINTER(_sz), ctypes.POINTER(_p)]),
     "dwt2d_workspace_bytes": (_sz, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),

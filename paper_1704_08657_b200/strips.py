@@ -195,3 +195,118 @@ def gpu_pair_fn(plan, stream=None):
     def fn(cur, top, bottom, out=None):
         return plan.forward_pair_strip(cur, top, bottom, out=out, stream=stream)
     return fn
+
+
+# ---------------------------------------------------------------------------
+# Device-side sharded pyramid (the library's in-C++ multi-GPU driver,
+# dwt2d_shard_* / dwt2d_forward_mallat_sharded): halo rows go straight into
+# the ring neighbours' exchange windows over peer memory; no host callback,
+# no collective library on the data path.
+
+class Shard:
+    """One rank of a row-strip sharded forward pyramid (dwt2d_shard) on the
+    current CUDA device."""
+
+    def __init__(self, plan, width: int, strip_height: int, levels: int, rank: int = 0, world: int = 1):
+        import ctypes
+        from . import native as N
+        self._N = N
+        self.plan = plan  # keeps the plan alive as long as the shard
+        self.width, self.strip_height, self.levels = width, strip_height, levels
+        self.rank, self.world = rank, world
+        h = ctypes.c_void_p()
+        N.check(N.lib.dwt2d_shard_create(plan._h, width, strip_height, levels, rank, world, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and getattr(self, "_N", None) is not None and self._N.lib is not None:
+            self._N.lib.dwt2d_shard_destroy(h)
+        self._h = None
+
+    def export(self) -> bytes:
+        """The exchange window's CUDA IPC handle (for ranks in other processes)."""
+        import ctypes
+        buf = ctypes.create_string_buffer(self._N.SHARD_HANDLE_BYTES)
+        self._N.check(self._N.lib.dwt2d_shard_export(self._h, buf, len(buf)))
+        return buf.raw
+
+    def connect(self, prev: "Shard", nxt: "Shard") -> None:
+        """Ring neighbours in this process (peer access is enabled)."""
+        self._N.check(self._N.lib.dwt2d_shard_connect(self._h, prev._h, nxt._h))
+
+    def connect_ipc(self, prev_handle: bytes, next_handle: bytes) -> None:
+        """Ring neighbours in other processes, from their export() handles."""
+        self._N.check(self._N.lib.dwt2d_shard_connect_ipc(self._h, prev_handle, next_handle))
+
+    def forward_mallat(self, strip, out=None, stream=None):
+        """Enqueue the whole strip pyramid (exchange included) on `stream`;
+        returns the strip-Mallat buffer."""
+        import torch
+        from .transform import _dev, _stream_handle
+        H, W = strip.shape
+        if out is None:
+            out = torch.empty((H, W), dtype=torch.float32, device=strip.device)
+        ptr, pitch = _dev(strip, "strip")
+        optr, opitch = _dev(out, "out")
+        self._N.check(self._N.lib.dwt2d_shard_forward_mallat(self._h, ptr, pitch, optr, opitch,
+                                                             _stream_handle(stream)))
+        return out
+
+    def status(self) -> int:
+        """0, or the exchange's error word (1: a neighbour never finished
+        the previous pyramid, 2: a halo never arrived)."""
+        import ctypes
+        v = ctypes.c_int()
+        self._N.check(self._N.lib.dwt2d_shard_status(self._h, ctypes.byref(v)))
+        return v.value
+
+
+def connect_ring(shards: Sequence["Shard"]) -> None:
+    """Connect shards of one process into a ring (rank order)."""
+    n = len(shards)
+    if n > 1:
+        for r, s in enumerate(shards):
+            s.connect(shards[(r - 1) % n], shards[(r + 1) % n])
+
+
+def dist_shard(plan, width: int, strip_height: int, levels: int, group=None) -> "Shard":
+    """This process's shard of a ring spanning the torch.distributed group:
+    creates it on the current device, exchanges the exchange-window handles
+    (all_gather_object over the group) and maps the neighbours' windows."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    sh = Shard(plan, width, strip_height, levels, rank, world)
+    if world > 1:
+        handles = [None] * world
+        dist.all_gather_object(handles, sh.export(), group=group)
+        prev, nxt = ring_neighbours(rank, world)
+        sh.connect_ipc(handles[prev], handles[nxt])
+        dist.barrier(group)
+    return sh
+
+
+def forward_mallat_sharded(plan, strips: Sequence, levels: int, outs=None, streams=None):
+    """Single-process multi-GPU pyramid (dwt2d_forward_mallat_sharded):
+    strips[r] is rank r's strip on its device (devices may repeat: virtual
+    ranks on one GPU). Returns the ranks' strip-Mallat buffers."""
+    import ctypes
+    import torch
+    from . import native as N
+    from .transform import _dev
+    n = len(strips)
+    H, W = strips[0].shape
+    if outs is None:
+        outs = [torch.empty((H, W), dtype=torch.float32, device=s.device) for s in strips]
+    sp = [_dev(s, "strip") for s in strips]
+    op = [_dev(o, "out") for o in outs]
+    devs = (ctypes.c_int * n)(*[s.device.index if s.device.index is not None else 0 for s in strips])
+    P = ctypes.c_void_p * n
+    S = ctypes.c_size_t * n
+    st = None
+    if streams is not None:
+        st = P(*[(s if isinstance(s, int) else s.cuda_stream) for s in streams])
+    N.check(N.lib.dwt2d_forward_mallat_sharded(plan._h, n, devs, P(*[p for p, _ in sp]), S(*[q for _, q in sp]),
+                                               W, H, levels, P(*[p for p, _ in op]), S(*[q for _, q in op]), st))
+    return outs

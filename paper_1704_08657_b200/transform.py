@@ -206,7 +206,7 @@ class Plan:
                     # the exchange's copies and P2P ops are ordered on the
                     # library's stream `st`: after the level that wrote
                     # `cur`, before the kernel that reads the halo rows
-                    with torch.cuda.stream(torch.cuda.ExternalStream(st, device=dev)):
+                    with torch.cuda.stream(torch.cuda.ExternalStream(st or 0, device=dev)):
                         exchange(_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
                                  _wrap(bottom, brows, w, hpitch, dev))
                     return 0
