@@ -1,31 +1,47 @@
 #!/usr/bin/env python3
 """Benchmark: CDF 9/7 forward 2-D DWT, Gpixel/s and HBM roofline on B200.
 
-Workload (BASELINE.json configs[3], the north-star target): non-separable
-lifting, optimized (paper's 36 ops/quad), CDF 9/7, float32, 8-level Mallat
-pyramid of a 16384 x 16384 image per GPU. One step = one full 8-level
-forward pyramid (8 fused level kernels) of the resident image.
-
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload auto|c3|c4]
 
-N > 1 (torchrun, one rank per GPU): weak scaling, each rank transforms its
-own 16384-row strip of a 16384 x (16384 N) image; rank 0 prints the line.
+Workloads (BASELINE.json): non-separable lifting, optimized (the paper's 36
+ops/quad), CDF 9/7, float32, 8-level Mallat pyramid, periodic extension.
+  c3  configs[3]: a 16384 x 16384 image (1 GiB). The N = 1 default.
+  c4  configs[4]: a 65536 x 65536 image (16 GiB), row-strip sharded over the
+      N ranks with the library's device-side halo exchange (dwt2d_shard_*:
+      each rank pushes its boundary rows into its ring neighbours' exchange
+      windows over NVLink, CUDA IPC between the rank processes). The N > 1
+      default: strong scaling of one fixed image, 65536 x 65536/N per GPU.
+With N > 1 (torchrun, one rank per GPU) c3 is strong-scaled the same way
+(16384 x 16384/N per GPU). One step = one full pyramid of the resident image
+(N > 1: every rank's strip pyramid, exchanges included).
 
 Timing: W untimed warm-up steps; the K timed steps are one CUDA graph
-(events around the dominant kernel on every 8th pyramid) replayed between a
-barrier + synchronize on both sides; CUDA events on the launching stream give
-the step time and the dominant kernel's duration (a separate untimed graph
-with an event after every level gives the per-level breakdown); max over
-ranks. The image is
-1 GiB, larger than the 126 MB L2, so the level-1 input always streams from
-HBM (no explicit flush). nvidia-smi samples clocks during the timed region.
+replayed between a barrier + synchronize on both sides, timed with CUDA
+events on the launching stream, max over ranks. Events around the dominant
+kernel (levels 1+2 fused) on every 8th step give its live duration (the
+roofline denominator); a separate untimed graph with events after every
+level (N > 1: around every push / interior / wait / border phase) gives the
+breakdown. Every input is >= 1 GiB per GPU at the defaults, larger than the
+126 MB L2, so level 1 always streams from HBM (no flush). nvidia-smi samples
+clocks during the timed region.
 
 Metric and traffic model: pixels of the original image per second, and the
 reference's own traffic model of 8 B per pixel per level (read + write
 float32, proj/src/bench.cpp:84-85), i.e. 10.667 B per original pixel for 8
 levels. roofline: the dominant launch — levels 1+2 fused in one pass
-(pair_engine.cuh; 8 B/pixel/level for both levels) or level 1 alone — over
-its measured duration vs the measured copy bandwidth in MEASURED_PEAKS.json.
+(pair_engine.cuh; 8 B/pixel/level for both levels) — over its measured
+duration vs the measured copy bandwidth in MEASURED_PEAKS.json.
+
+e2e: the same pyramid through the public entry point with host buffers:
+N = 1 dwt2d_forward_mallat_host (pinned host image in, pyramid out, the
+copies overlapped with level 1 by row bands); N > 1 per rank: pinned host
+strip -> H2D -> dwt2d_shard_forward_mallat -> D2H.
+
+cpu_baseline / --impl reference: the reference's own CPU path (oracle/_ref:
+the unmodified reference sources compiled with its Release flags) on this
+box's host cores: the full 16384^2 image, 8-level Mallat loop over its
+compile/run API, all cores (and a workers=1 leg on a declared row band).
 """
 from __future__ import annotations
 
@@ -43,21 +59,26 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 WAVELET, SCHEME, OPTIMIZED = "cdf97", "nonseparable-lifting", True
-SIZE, LEVELS = 16384, 8
+LEVELS = 8
+WORKLOADS = {"c3": (16384, "BASELINE configs[3]"), "c4": (65536, "BASELINE configs[4]")}
 METRIC = "CDF 9/7 2-D DWT Gpixel/s (ns/pixel) and achieved HBM GB/s vs peak, 1/2/4/8 GPU"
 EVENT_STRIDE = 8  # timed pyramids per sampled dominant-kernel duration
-# CPU baseline sample: a 16384 x 2048 row band of the same image, 8 levels
-SAMPLE_ROWS = 2048
+# CPU baseline: the full 16384^2 image on all cores; the workers=1 leg on a
+# 16384 x BAND_ROWS row band of it (a full single-thread run takes ~30 s)
+BAND_ROWS = 1024
 
 
-def workload_config(n):
+def workload_config(wl, n):
+    size, which = WORKLOADS[wl]
     return {
         "workload": f"CDF 9/7 non-separable lifting (optimized, 36 ops/quad) forward 8-level Mallat "
-                    f"pyramid, {SIZE}x{SIZE} float32 per GPU (BASELINE configs[3])",
+                    f"pyramid, {size}x{size} float32 ({which})" +
+                    (f", row-strip sharded: {size}x{size // n} per GPU" if n > 1 else ""),
         "wavelet": WAVELET, "scheme": SCHEME, "optimized": OPTIMIZED,
-        "image": [SIZE, SIZE * n], "levels": LEVELS, "extension": "periodic",
-        "parallelism": f"row-strips x{n}" if n > 1 else "single GPU",
-        "l2": "inputs larger than L2 (1 GiB image per GPU vs 126 MB L2), no flush",
+        "image": [size, size], "levels": LEVELS, "extension": "periodic",
+        "parallelism": (f"row strips x{n}, device-side halo exchange over NVLink (CUDA IPC peer stores)"
+                        if n > 1 else "single GPU"),
+        "l2": f"inputs larger than L2 ({size * size * 4 // n >> 20} MiB per GPU vs 126 MB L2), no flush",
         "traffic_model": "8 B/pixel/level (reference bench.cpp:84-85)",
     }
 
@@ -137,57 +158,80 @@ def dist_setup():
     return n, rank, local
 
 
-def cpu_reference(steps, warmup, workers=None):
-    """Reference CPU implementation (oracle/_ref, compiled from the reference
-    sources) on a bounded sample: a 16384 x SAMPLE_ROWS band, 8 levels."""
+def cpu_reference(img_rows, repeats, workers):
+    """Median seconds of the reference's own path (oracle/_ref: compile/run
+    over the 8-level Mallat loop, run_bench semantics bench.cpp:28-44: one
+    warm-up, then `repeats` timed runs) on the first `img_rows` rows of the
+    16384-wide LCG image."""
     from oracle import ref as R
     from oracle import dwt_oracle as O
-    workers = workers or os.cpu_count() or 1
-    img = O.random_image(SIZE, SAMPLE_ROWS, 1)
-    times = []
-    for i in range(warmup + steps):
-        t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=workers, repeats=1)
-        if i >= warmup:
-            times.append(t)
-    t = statistics.median(times)
-    gpix = SIZE * SAMPLE_ROWS / t / 1e9
-    return {"value": gpix, "unit": "Gpixel/s", "cores": workers, "kind": "reference",
-            "sample": f"{SIZE}x{SAMPLE_ROWS} band of the LCG image, {LEVELS}-level Mallat loop over the "
-                      f"reference compile/run API (oracle/_ref, reference sources, -O3), workers={workers}, "
-                      f"median of {len(times)}", "seconds": t}
+    img = O.random_image(16384, img_rows, 1)
+    t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=workers, repeats=repeats)
+    return t
 
 
-def run_reference_arm(args):
+def cpu_baseline_leg():
+    """cpu_baseline of the N = 1 line: the full configs[3] image on every host
+    core (median of 5 after a warm-up) plus a workers = 1 leg on a band."""
+    cores = os.cpu_count() or 1
+    t = cpu_reference(16384, 5, cores)
+    t1 = cpu_reference(BAND_ROWS, 5, 1)
+    return {"value": 16384 * 16384 / t / 1e9, "unit": "Gpixel/s", "cores": cores, "kind": "reference",
+            "sample": f"full 16384x16384 LCG image (seed 1), 8-level Mallat loop over the reference "
+                      f"compile/run API (oracle/_ref: reference sources, -O3), workers={cores}, one warm-up + "
+                      f"median of 5 ({t:.2f} s per pyramid)",
+            "workers_1": {"value": 16384 * BAND_ROWS / t1 / 1e9, "unit": "Gpixel/s", "cores": 1,
+                          "sample": f"16384x{BAND_ROWS} row band of the same image, 8 levels, workers=1, "
+                                    f"one warm-up + median of 5 ({t1:.2f} s per pyramid)"}}
+
+
+def run_reference_arm(args, wl):
+    """--impl reference: the reference's CPU path with every host thread, on
+    this arm's workload (rank 0 only). configs[3]: the whole 16384^2 image
+    per step; configs[4] (16 GiB image, more than the reference's ~4 copies
+    fit in host RAM): a declared 65536 x 2048 row band per step (the
+    reference's per-pixel rate)."""
     n, rank, _ = dist_setup()
     if rank != 0:
         return 0
-    cb = cpu_reference(args.steps, args.warmup)
-    v = cb["value"]
+    from oracle import ref as R
+    from oracle import dwt_oracle as O
+    cores = os.cpu_count() or 1
+    size = WORKLOADS[wl][0]
+    rows = size if wl == "c3" else 2048
+    img = O.random_image(size, rows, 1)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=cores, repeats=1)
+        if i >= args.warmup:
+            times.append(t)
+    t = statistics.median(times)
+    v = size * rows / t / 1e9
+    sample = (f"{'full ' if rows == size else ''}{size}x{rows} {'image' if rows == size else 'row band of the image'}"
+              f" (LCG seed 1), 8-level Mallat loop over the reference compile/run API (oracle/_ref, reference "
+              f"sources, -O3), workers={cores}, median of {len(times)} steps after {args.warmup} warm-up")
     line = {
         "metric": METRIC, "value": v, "unit": "Gpixel/s", "n_gpus": n, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference LCG image, seed 1)",
-        "config": workload_config(n), "impl": "reference",
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong" if n > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference LCG image, seed 1)", "config": workload_config(wl, n), "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "Gpixel/s", "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-UP = DOWN = 2  # CDF 9/7 level reach in component rows (halo = 4 image rows each side)
-
-
 def run_single(args, plan, img, out, dev):
     """N = 1: K pyramids (forward_mallat, the library's multi-level entry
-    point) captured in one CUDA graph. The dominant kernel (levels 1+2 fused,
-    or level 1) is bracketed by events on every EVENT_STRIDE-th pyramid of the
-    timed graph (its mean duration is the roofline denominator); a second,
-    untimed graph with an event after every level gives the breakdown."""
+    point) captured in one CUDA graph. The dominant kernel (levels 1+2 fused)
+    is bracketed by events on every EVENT_STRIDE-th pyramid of the timed
+    graph (its mean duration is the roofline denominator); a second, untimed
+    graph with an event after every level gives the breakdown."""
     import torch
     import paper_1704_08657_b200 as dwt
     from paper_1704_08657_b200.native import Event
-    W = H = SIZE
+    H, W = img.shape
     scratch = torch.empty(dwt.workspace_bytes(W, H, LEVELS) // 4 + 64, dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
 
@@ -206,117 +250,108 @@ def run_single(args, plan, img, out, dev):
                 step(evs)
         return g
 
-    # the dominant kernel's duration is sampled live inside the timed region on
-    # every EVENT_STRIDE-th pyramid: an event node between two kernels breaks
-    # their programmatic (PDL) overlap, ~7 us per pyramid if every step had one
+    # an event node between two kernels breaks their programmatic (PDL)
+    # overlap (~7 us per pyramid if every step had one): sample every 8th
     timed_events = [([Event(), Event()] + [None] * (LEVELS - 1)) if k % EVENT_STRIDE == 0 else None
                     for k in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if args.launch == "graph":
-        launches0 = dwt.launch_count()
-        graph = capture(timed_events)
-        launches = dwt.launch_count() - launches0
-        with torch.cuda.stream(stream):
-            graph.replay()  # untimed replay warms the graph
-        torch.cuda.synchronize()
-        with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
-            t0.record(stream)
-            graph.replay()  # replays on the current stream (= `stream` here)
-            t1.record(stream)
-            t1.synchronize()
-    else:  # eager: the library's calls as a user makes them (levels chained by PDL)
-        torch.cuda.synchronize()
-        launches0 = dwt.launch_count()
-        with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
-            t0.record(stream)
-            for evs in timed_events:
-                step(evs)
-            t1.record(stream)
-            t1.synchronize()
-        launches = dwt.launch_count() - launches0
+    launches0 = dwt.launch_count()
+    graph = capture(timed_events)
+    launches = dwt.launch_count() - launches0
+    with torch.cuda.stream(stream):
+        graph.replay()  # untimed replay warms the graph
+    torch.cuda.synchronize()
+    with ClockSampler(0 if dev.index is None else dev.index) as clk, torch.cuda.stream(stream):
+        t0.record(stream)
+        graph.replay()
+        t1.record(stream)
+        t1.synchronize()
     torch.cuda.synchronize()
     ms_per_step = t0.elapsed_time(t1) / args.steps
-    level1_ms = statistics.mean(e[0].elapsed_ms(e[1]) for e in timed_events if e is not None)
+    dom_ms = statistics.mean(e[0].elapsed_ms(e[1]) for e in timed_events if e is not None)
 
-    # breakdown pass (not part of the timed region)
-    nb = min(args.steps, 50)
+    nb = min(args.steps, 50)  # breakdown pass (not part of the timed region)
     all_events = [[Event() for _ in range(LEVELS + 1)] for _ in range(nb)]
     g2 = capture(all_events)
     with torch.cuda.stream(stream):
         g2.replay()
     torch.cuda.synchronize()
     level_ms = [statistics.mean(e[l].elapsed_ms(e[l + 1]) for e in all_events) for l in range(LEVELS)]
-    level_ms[0] = level1_ms
-    return SIZE * SIZE / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
+    level_ms[0] = dom_ms
+    fused12 = launches == args.steps * (LEVELS - 1)
+    return {"ms_per_step": ms_per_step, "dom_ms": dom_ms, "fused12": fused12,
+            "levels_ms": [round(x, 5) for x in level_ms], "launches": launches, "clk": clk}
 
 
-def run_sharded(args, plan, img, out, dev, n):
-    """N > 1: each rank owns a 16384-row strip. The library's strip driver
-    (dwt2d_forward_mallat_strip, C++) runs the pyramid: levels 1+2 as one
-    fused pass from 12+12 halo rows, every later level from 4+4 rows, the
-    rows coming from the ring neighbours through the exchange callback
-    (NCCL batched send/recv). The timed region is K such pyramids; an
-    untimed pass of the Python per-kernel path with events gives the
-    per-kernel breakdown."""
+def run_sharded(args, plan, shard, img, out, dev, n):
+    """N > 1: every rank's strip pyramid (dwt2d_shard_forward_mallat: halo
+    pushes into the ring neighbours' windows, interior rows, device-side
+    waits, border rows; levels 1+2 fused) — K of them in one CUDA graph per
+    rank, replayed between barriers; max over ranks. An untimed graph with
+    events around every phase gives the per-step breakdown (push, interior,
+    wait, border) and the dominant kernel's duration."""
     import torch
     import torch.distributed as dist
     import paper_1704_08657_b200 as dwt
-    from paper_1704_08657_b200 import strips as S
-    ex = S.HaloExchange()
-    H, W = img.shape
-    scratch = torch.empty(dwt.native.lib.dwt2d_strip_workspace_bytes(plan._h, W, H, LEVELS) // 4 + 64,
-                          dtype=torch.float32, device=dev)
+    from paper_1704_08657_b200.native import Event
+    stream = torch.cuda.Stream(device=dev)
+    nsteps = shard.info()["steps"]
 
-    def step():
-        S.gpu_forward_mallat(plan, img, LEVELS, exchange=ex, out=out, scratch=scratch)
+    def step(events=None):
+        shard.forward_mallat(img, out=out, stream=stream.cuda_stream, events=events)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches0 = dwt.launch_count()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev.index or 0) as clk:
-        t0.record()
-        for _ in range(args.steps):
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
             step()
-        t1.record()
-        t1.synchronize()
+    stream.synchronize()
+    dist.barrier()
+
+    def capture(event_sets):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for evs in event_sets:
+                step(evs)
+        return g
+
+    launches0 = dwt.launch_count()
+    graph = capture([None] * args.steps)
+    launches = dwt.launch_count() - launches0
+    with torch.cuda.stream(stream):
+        graph.replay()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk, torch.cuda.stream(stream):
         dist.barrier()
         torch.cuda.synchronize()
-    launches = dwt.launch_count() - launches0
+        t0.record(stream)
+        graph.replay()
+        t1.record(stream)
+        t1.synchronize()
+    dist.barrier()
     total = torch.tensor([t0.elapsed_time(t1)], device=dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
 
-    # breakdown (untimed): the same kernels through the Python strip path
-    cur_events = []
-
-    def timed(fn):
-        def w(cur, top, bottom, out=None):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            r = fn(cur, top, bottom, out=out)
-            e1.record()
-            cur_events.append((e0, e1))
-            return r
-        return w
-
-    pf = S.gpu_pair_fn(plan)
-    pair = pf is not None and os.environ.get("DWT2D_PAIR", "1") != "0"
-    nb = min(args.steps, 20)
-    scratch_out = torch.empty_like(out)
-    for _ in range(nb):
-        S.forward_mallat_strips(timed(S.gpu_level_fn(plan)), img, LEVELS, UP, DOWN, ex, out=scratch_out,
-                                pair_fn=timed(pf) if pair else None)
+    nb = min(args.steps, 20)  # breakdown (untimed)
+    evs = [[Event() for _ in range(1 + 4 * nsteps)] for _ in range(nb)]
+    g2 = capture(evs)
+    with torch.cuda.stream(stream):
+        g2.replay()
     torch.cuda.synchronize()
-    per = LEVELS - 1 if pair else LEVELS  # kernels per pyramid
-    kern_ms = [statistics.mean(cur_events[k * per + l][0].elapsed_time(cur_events[k * per + l][1])
-                               for k in range(nb)) for l in range(per)]
-    level_ms = [kern_ms[0], 0.0] + kern_ms[1:] if pair else kern_ms
-    assert torch.equal(scratch_out, out), "strip driver and Python strip path disagree"
-    return SIZE * SIZE * n / (ms_per_step * 1e-3) / 1e9, ms_per_step, level_ms, launches, clk
+
+    def span(a, b):
+        return statistics.mean(e[a].elapsed_ms(e[b]) for e in evs)
+    phases = []
+    for k in range(nsteps):
+        b = 1 + 4 * k
+        phases.append({"push": span(b - 1, b), "interior": span(b, b + 1), "wait": span(b + 1, b + 2),
+                       "border": span(b + 2, b + 3)})
+    step_ms = [round(sum(p.values()), 5) for p in phases]
+    dom_ms = sum(phases[0][k] for k in ("interior", "border"))  # the fused level pair's launches
+    exch_us = 1e3 * sum(p["push"] + p["wait"] for p in phases)
+    return {"ms_per_step": ms_per_step, "dom_ms": dom_ms, "fused12": shard.info()["pair"],
+            "levels_ms": step_ms, "launches": launches, "clk": clk, "phases": phases, "exchange_us": exch_us}
 
 
 def main():
@@ -325,29 +360,30 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "c3", "c4"],
+                    help="c3: 16384^2 (BASELINE configs[3]), c4: 65536^2 (configs[4]); auto: c3 at N=1, c4 at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
-                    help="timed region: one CUDA graph of K pyramids, or K eager library calls")
     ap.add_argument("--sharded", action="store_true",
-                    help="run the N>1 strip path (halo exchange + strip kernels) even at N=1 (testing)")
+                    help="run the N>1 sharded path (ring of one at N=1; testing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    n, rank, local = dist_setup()
+    wl = args.workload if args.workload != "auto" else ("c3" if n == 1 else "c4")
     if args.impl == "reference":
-        return run_reference_arm(args)
+        return run_reference_arm(args, wl)
 
     import torch
     import torch.distributed as dist
     import paper_1704_08657_b200 as dwt
+    from paper_1704_08657_b200 import strips as S
     from paper_1704_08657_b200.synth import random_image
 
     # stdout carries exactly one JSON line (rank 0): everything else written
-    # to fd 1 — e.g. the "NCCL version" banner printed when the first
-    # communicator is created — goes to stderr
+    # to fd 1 (e.g. the NCCL banner) goes to stderr
     json_out = os.fdopen(os.dup(1), "w")
     sys.stdout.flush()
     os.dup2(2, 1)
-    n, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sharded = n > 1 or args.sharded
@@ -361,18 +397,21 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     plan = dwt.Plan(WAVELET, SCHEME, optimized=OPTIMIZED)
-    W = H = SIZE
-    # this rank's strip: rows [rank*H, (rank+1)*H) of the W x (n*H) image
-    img = random_image(W, H * n, 1, row0=rank * H, rows=H, device=dev)
+    size = WORKLOADS[wl][0]
+    W, Hs = size, size // n
+    # this rank's strip: rows [rank*Hs, (rank+1)*Hs) of the size x size image
+    img = random_image(W, size, 1, row0=rank * Hs, rows=Hs, device=dev)
     out = torch.empty_like(img)
+    shard = None
     if sharded:
-        value, ms_per_step, level_ms, launches_captured, clk = run_sharded(args, plan, img, out, dev, n)
+        shard = S.dist_shard(plan, W, Hs, LEVELS)
+        r = run_sharded(args, plan, shard, img, out, dev, n)
     else:
-        value, ms_per_step, level_ms, launches_captured, clk = run_single(args, plan, img, out, dev)
-    pixels = W * H * n
+        r = run_single(args, plan, img, out, dev)
+    pixels = size * size
+    value = pixels / (r["ms_per_step"] * 1e-3) / 1e9
 
-    # end to end through the C ABI host entry point: pinned host image ->
-    # H2D -> 8 levels -> D2H of the whole pyramid, synchronous per step
+    # end to end through the public entry point with host buffers
     host_img = img.cpu().pin_memory()
     host_out = torch.empty_like(host_img).pin_memory()
     if not sharded:
@@ -381,13 +420,11 @@ def main():
         def e2e_step():
             plan.forward_mallat_host(hi, LEVELS, ho)
     else:
-        from paper_1704_08657_b200 import strips as S
-        ex = S.HaloExchange()
         dev_in, dev_out = torch.empty_like(img), torch.empty_like(img)
 
         def e2e_step():
             dev_in.copy_(host_img, non_blocking=True)
-            S.gpu_forward_mallat(plan, dev_in, LEVELS, exchange=ex, out=dev_out)
+            shard.forward_mallat(dev_in, out=dev_out)
             host_out.copy_(dev_out, non_blocking=True)
             torch.cuda.current_stream().synchronize()
     e2e_step()
@@ -395,6 +432,8 @@ def main():
         dist.barrier()
     e2e_t = []
     for _ in range(args.e2e_steps):
+        if sharded:
+            dist.barrier()
         a = time.perf_counter()
         e2e_step()
         e2e_t.append(time.perf_counter() - a)
@@ -403,55 +442,61 @@ def main():
         t = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    assert torch.equal(host_out.to(dev), out), "end-to-end entry point disagrees with device pyramid"
+    assert torch.equal(host_out.to(dev), out), "end-to-end entry point disagrees with the device pyramid"
 
     if rank == 0:
         peak, peak_src = peaks()
-        # the dominant kernel: level 1, or levels 1+2 fused in one pass
-        # (pair_engine.cuh: one launch fewer per pyramid, the first event
-        # pair then brackets both levels)
-        fused12 = launches_captured == args.steps * (LEVELS - 1)
-        l1_bytes = 8.0 * W * H * (1.25 if fused12 else 1.0)
-        achieved = l1_bytes / (level_ms[0] * 1e-3) / 1e9
-        kernel_desc = ("levels 1+2 fused (16384^2 -> LL_2 + 6 detail bands, LL_1 kept on chip), "
-                       "8 B/pixel/level algorithmic" if fused12 else
-                       "level 1 (16384^2 -> 4 x 8192^2), 8 B/pixel algorithmic")
-        pyr_bytes = sum(8.0 * (W >> l) * (H >> l) for l in range(LEVELS))
+        dom_bytes = 8.0 * W * Hs * (1.25 if r["fused12"] else 1.0)
+        achieved = dom_bytes / (r["dom_ms"] * 1e-3) / 1e9
+        kernel_desc = (f"levels 1+2 fused ({W}x{Hs} -> LL_2 + 6 detail bands, LL_1 kept on chip), "
+                       "8 B/pixel/level algorithmic" if r["fused12"] else
+                       f"level 1 ({W}x{Hs}), 8 B/pixel algorithmic")
+        pyr_bytes = sum(8.0 * (W >> l) * (Hs >> l) for l in range(LEVELS))
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and n == 1:
             try:
-                cb = cpu_reference(steps=3, warmup=1)
-                cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                cpu = cpu_baseline_leg()
             except Exception as e:  # oracle not built on this box
                 cpu = {"value": None, "unit": "Gpixel/s", "cores": 0, "kind": "reference",
                        "sample": f"unavailable: {e}"}
         line = {
             "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": n, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if n > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference LCG random_image, seed 1, generated on device with jump-ahead)",
-            "config": workload_config(n),
-            "ns_per_pixel": ms_per_step * 1e6 / pixels,
-            "pyramid_hbm_gbs_per_gpu": pyr_bytes / (ms_per_step * 1e-3) / 1e9,
-            "levels_ms": [round(x, 5) for x in level_ms],
+            "config": workload_config(wl, n),
+            "ns_per_pixel": r["ms_per_step"] * 1e6 / pixels,
+            "pyramid_hbm_gbs_per_gpu": pyr_bytes / (r["ms_per_step"] * 1e-3) / 1e9,
+            "levels_ms": r["levels_ms"],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic("ncu_pair_summary.json" if fused12 else "ncu_level1_summary.json"),
-                         "algorithmic_bytes": l1_bytes,
-                         "kernel": kernel_desc, "peak_source": peak_src},
+                         "traffic": ncu_traffic("ncu_pair_summary.json" if r["fused12"] else "ncu_level1_summary.json")
+                         if (wl == "c3" and n == 1) else None,
+                         "algorithmic_bytes": dom_bytes, "kernel": kernel_desc, "peak_source": peak_src},
             "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
-                    "h2d_bytes_per_step": int(W * H * 4), "d2h_bytes_per_step": int(W * H * 4),
+                    "h2d_bytes_per_step": int(W * Hs * 4), "d2h_bytes_per_step": int(W * Hs * 4),
                     "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if not sharded else
-                            "pinned host strip -> H2D -> dwt2d_forward_mallat_strip (C ABI strip "
-                            "pyramid driver, NCCL halo callback) -> D2H, per rank")},
-            "gpu_launches": int(launches_captured),
-            "halo_exchange": ("NCCL batched send/recv per rank (ring): 12+12 image rows for the fused "
-                              "levels 1+2, 4+4 rows for each later level" if sharded else None),
-            "clocks": clk.summary(),
+                            "per rank: pinned host strip -> H2D -> dwt2d_shard_forward_mallat (C ABI, device-side "
+                            "halo exchange) -> D2H; bytes per rank, time max over ranks")},
+            "gpu_launches": int(r["launches"]),
+            "clocks": r["clk"].summary(),
             "cpu_baseline": cpu,
         }
+        if sharded:
+            info = shard.info()
+            line["halo_exchange"] = {
+                "mechanism": "device-side: peer stores into the ring neighbours' exchange windows "
+                             "(CUDA IPC), release/acquire counters, interior rows overlapped",
+                "bytes_per_rank_per_pyramid": info["halo_bytes"],
+                "exchange_steps": info["steps"],
+                "push_plus_wait_us_per_pyramid": round(r["exchange_us"], 2),
+                "phases_ms_step0": {k: round(v, 5) for k, v in r["phases"][0].items()},
+            }
+            line["levels_ms_note"] = "per exchange step (levels 1+2 fused, then one level each): push+interior+wait+border"
         print(json.dumps(line), file=json_out, flush=True)
     if sharded:
+        dist.barrier()
+        del shard
         dist.destroy_process_group()
     return 0
 

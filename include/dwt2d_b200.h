@@ -249,6 +249,16 @@ DWT2D_B200_API int dwt2d_shard_connect_ipc(dwt2d_shard* shard, const void* prev_
                                            const void* next_handle);
 DWT2D_B200_API int dwt2d_shard_forward_mallat(dwt2d_shard* shard, const float* strip, size_t pitch,
                                               float* out, size_t out_pitch, void* stream);
+/* the same with CUDA events (dwt2d_event_create; NULL entries allowed):
+ * events[0] before the first push; for exchange step e (the fused levels 1+2
+ * or one level) events[1 + 4e + k] after its push (k = 0), interior rows
+ * (1), wait (2) and border rows (3). 1 + 4 * steps entries. */
+DWT2D_B200_API int dwt2d_shard_forward_mallat_ex(dwt2d_shard* shard, const float* strip, size_t pitch,
+                                                 float* out, size_t out_pitch, void* const* events,
+                                                 void* stream);
+/* exchange steps per pyramid, whether the first fuses levels 1+2, and the
+ * halo bytes this rank pushes to its neighbours per pyramid */
+DWT2D_B200_API int dwt2d_shard_info(const dwt2d_shard* shard, int* steps, int* pair, size_t* halo_bytes);
 DWT2D_B200_API int dwt2d_shard_status(const dwt2d_shard* shard, int* error);
 /* Single-process driver over `nranks` ranks on `devices` (a device may
  * repeat: virtual ranks on one GPU): strips[r] / out[r] live on devices[r];

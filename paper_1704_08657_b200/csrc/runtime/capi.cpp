@@ -1768,21 +1768,45 @@ int dwt2d_shard_connect_ipc(dwt2d_shard* s, const void* prev_handle, const void*
   });
 }
 
-int dwt2d_shard_forward_mallat(dwt2d_shard* s, const float* strip, size_t pitch, float* out, size_t out_pitch,
-                               void* stream) {
+int dwt2d_shard_forward_mallat_ex(dwt2d_shard* s, const float* strip, size_t pitch, float* out, size_t out_pitch,
+                                  void* const* events, void* stream) {
   return guard([&] {
     if (!s) fail(DWT2D_EINVAL, "null argument");
     check_shard_args(*s, strip, out);
     DeviceGuard g(s->device);
     const cudaStream_t st = as_stream(stream);
+    if (events) record(events[0], st);
     for (size_t e = 0; e < s->steps.size(); ++e) {
+      void* const* ev = events ? events + 1 + 4 * e : nullptr;
       const StepIO io = step_input(*s, e, strip, pitch, out, out_pitch);
       shard_push(*s, e, io, st);
+      if (ev) record(ev[0], st);
       shard_compute(*s, e, io, out, out_pitch, 0, st);
+      if (ev) record(ev[1], st);
       shard_wait(*s, st);
+      if (ev) record(ev[2], st);
       shard_compute(*s, e, io, out, out_pitch, 1, st);
+      if (ev) record(ev[3], st);
     }
     shard_done(*s, st);
+  });
+}
+
+int dwt2d_shard_forward_mallat(dwt2d_shard* s, const float* strip, size_t pitch, float* out, size_t out_pitch,
+                               void* stream) {
+  return dwt2d_shard_forward_mallat_ex(s, strip, pitch, out, out_pitch, nullptr, stream);
+}
+
+int dwt2d_shard_info(const dwt2d_shard* s, int* steps, int* pair, size_t* halo_bytes) {
+  return guard([&] {
+    if (!s) fail(DWT2D_EINVAL, "null argument");
+    if (steps) *steps = int(s->steps.size());
+    if (pair) *pair = !s->steps.empty() && s->steps[0].pair ? 1 : 0;
+    if (halo_bytes) {  // bytes this rank pushes to its neighbours per pyramid
+      size_t b = 0;
+      for (const ExchangeStep& x : s->steps) b += size_t(x.trows + x.brows) * size_t(x.width) * sizeof(float);
+      *halo_bytes = b;
+    }
   });
 }
 

@@ -110,6 +110,9 @@ _SIGS = {
     "dwt2d_shard_connect_ipc": (ctypes.c_int, [_p, ctypes.c_char_p, ctypes.c_char_p]),
     "dwt2d_shard_forward_mallat": (ctypes.c_int, [_p, _p, _sz, _p, _sz, _p]),
     "dwt2d_shard_status": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int)]),
+    "dwt2d_shard_forward_mallat_ex": (ctypes.c_int, [_p, _p, _sz, _p, _sz, ctypes.POINTER(ctypes.c_void_p), _p]),
+    "dwt2d_shard_info": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(_sz)]),
     "dwt2d_forward_mallat_sharded": (ctypes.c_int, [_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                                     ctypes.POINTER(_p), ctypes.POINTER(_sz), ctypes.c_int,
                                                     ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p),

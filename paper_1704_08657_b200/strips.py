@@ -239,9 +239,11 @@ class Shard:
         """Ring neighbours in other processes, from their export() handles."""
         self._N.check(self._N.lib.dwt2d_shard_connect_ipc(self._h, prev_handle, next_handle))
 
-    def forward_mallat(self, strip, out=None, stream=None):
+    def forward_mallat(self, strip, out=None, stream=None, events=None):
         """Enqueue the whole strip pyramid (exchange included) on `stream`;
-        returns the strip-Mallat buffer."""
+        returns the strip-Mallat buffer. events: None, or 1 + 4 * steps
+        native.Event / None entries (dwt2d_shard_forward_mallat_ex)."""
+        import ctypes
         import torch
         from .transform import _dev, _stream_handle
         H, W = strip.shape
@@ -249,9 +251,23 @@ class Shard:
             out = torch.empty((H, W), dtype=torch.float32, device=strip.device)
         ptr, pitch = _dev(strip, "strip")
         optr, opitch = _dev(out, "out")
-        self._N.check(self._N.lib.dwt2d_shard_forward_mallat(self._h, ptr, pitch, optr, opitch,
-                                                             _stream_handle(stream)))
+        if events is None:
+            self._N.check(self._N.lib.dwt2d_shard_forward_mallat(self._h, ptr, pitch, optr, opitch,
+                                                                 _stream_handle(stream)))
+        else:
+            if len(events) != 1 + 4 * self.info()["steps"]:
+                raise ValueError("events needs 1 + 4 * steps entries")
+            arr = (ctypes.c_void_p * len(events))(*[None if e is None else e.handle for e in events])
+            self._N.check(self._N.lib.dwt2d_shard_forward_mallat_ex(self._h, ptr, pitch, optr, opitch, arr,
+                                                                    _stream_handle(stream)))
         return out
+
+    def info(self) -> dict:
+        import ctypes
+        steps, pair, hb = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+        self._N.check(self._N.lib.dwt2d_shard_info(self._h, ctypes.byref(steps), ctypes.byref(pair),
+                                                   ctypes.byref(hb)))
+        return {"steps": steps.value, "pair": bool(pair.value), "halo_bytes": hb.value}
 
     def status(self) -> int:
         """0, or the exchange's error word (1: a neighbour never finished

@@ -203,12 +203,20 @@ class Plan:
             def _cb(user, cur, cpitch, w, h, top, bottom, hpitch, trows, brows, st):
                 try:
                     dev = strip.device
-                    # the exchange's copies and P2P ops are ordered on the
-                    # library's stream `st`: after the level that wrote
-                    # `cur`, before the kernel that reads the halo rows
-                    with torch.cuda.stream(torch.cuda.ExternalStream(st or 0, device=dev)):
-                        exchange(_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
-                                 _wrap(bottom, brows, w, hpitch, dev))
+                    args = (_wrap(cur, h, w, cpitch, dev), trows, brows, _wrap(top, trows, w, hpitch, dev),
+                            _wrap(bottom, brows, w, hpitch, dev))
+                    cur_stream = torch.cuda.current_stream(dev)
+                    if (st or 0) == cur_stream.cuda_stream:
+                        exchange(*args)
+                    else:
+                        # the exchange's copies and P2P ops run on torch's
+                        # current stream: after the level the library
+                        # enqueued on `st` that wrote `cur`, and before the
+                        # kernel on `st` that reads the halo rows
+                        lib_stream = torch.cuda.ExternalStream(st, device=dev)
+                        cur_stream.wait_stream(lib_stream)
+                        exchange(*args)
+                        lib_stream.wait_stream(cur_stream)
                     return 0
                 except Exception:  # surfaced as DWT2D_EINVAL by the library
                     import traceback

@@ -232,8 +232,8 @@ def test_gpu_strip_kernels_equal_single_gpu_pyramid(cuda, world, wavelet, scheme
 @pytest.mark.parametrize("wavelet,scheme,opt", [("cdf97", "nonseparable-lifting", True),
                                                 ("cdf53", "separable-lifting", False),
                                                 ("dd137", "nonseparable-lifting", True)])
-@pytest.mark.parametrize("pair", ["1", "0"])
-def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, pair):
+@pytest.mark.parametrize("pair,own_stream", [("1", False), ("0", False), ("1", True)])
+def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme, opt, pair, own_stream):
     """The C++ strip-pyramid driver (dwt2d_forward_mallat_strip) with a
     Python halo-exchange callback reproduces the single-GPU pyramid bit for
     bit: world 1 without a callback (periodic wrap inside the strip), 2 and
@@ -262,7 +262,12 @@ def test_gpu_strip_driver_equals_single_gpu_pyramid(cuda, world, wavelet, scheme
                 top.copy_(t)
                 bottom.copy_(b)
             strip = img[rank * Hs:(rank + 1) * Hs].contiguous()
-            outs[rank] = S.gpu_forward_mallat(plan, strip, L, exchange=fill)
+            # own_stream: the library runs on a stream that is not torch's
+            # current one; the callback's copies must still be ordered with it
+            st = torch.cuda.Stream() if own_stream else None
+            if st is not None:
+                st.wait_stream(torch.cuda.current_stream())
+            outs[rank] = S.gpu_forward_mallat(plan, strip, L, exchange=fill, stream=st)
             torch.cuda.synchronize()
         except Exception as e:  # surfaced below
             errors.append(e)
