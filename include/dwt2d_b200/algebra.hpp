@@ -67,7 +67,10 @@ struct Term {
 
 enum class Axis { horizontal, vertical };
 
-// Sparse bivariate Laurent polynomial; terms sorted by (m, n), no zeros.
+// Bivariate Laurent polynomial. Stored as a dense coefficient grid over its
+// bounding box — every cell (m, n) of [m0, m0 + w) x [n0, n0 + h) is either
+// a term or empty — plus the key-sorted term list of the occupied cells
+// (terms()). Zero coefficients are never stored.
 class LaurentPoly {
  public:
   LaurentPoly() = default;
@@ -95,7 +98,14 @@ class LaurentPoly {
   }
 
  private:
-  std::vector<Term> t_;
+  friend class TermGrid;
+  struct Cell {
+    bool used = false;
+    Coeff c;
+  };
+  int m0_ = 0, n0_ = 0, w_ = 0, h_ = 0;
+  std::vector<Cell> grid_;  // (m - m0) * h + (n - n0): m-major, the key order
+  std::vector<Term> t_;     // the occupied cells in grid order
 };
 
 LaurentPoly transpose(const LaurentPoly& p);

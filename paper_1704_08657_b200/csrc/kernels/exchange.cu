@@ -55,12 +55,16 @@ __device__ bool spin_until(const unsigned* flag, unsigned target, unsigned long 
   while (int(ld_acquire_sys(flag) - target) < 0) {
     if (global_ns() - t0 > timeout_ns) return false;
     __nanosleep(ns);
-    ns = ns < 1024 ? ns * 2 : ns;
+    ns = ns < 256 ? ns * 2 : ns;
   }
   return true;
 }
 
 __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ HaloPushArgs a) {
+  // PDL: resident during the previous level's tail; its LL rows (this
+  // push's source) are complete after the wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   if (a.first_step) {
     // the neighbours must have finished the previous pyramid (stopped
     // reading the halo buffers this push overwrites)
@@ -110,6 +114,15 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
       __threadfence_system();
       red_release_sys(a.flag_next, 1u);
       red_release_sys(a.flag_prev, 1u);
+      if (a.wait_after) {
+        const unsigned st = a.seen[0] + 1u, sb = a.seen[1] + 1u;
+        if (!spin_until(a.my_top, st, a.timeout_ns) || !spin_until(a.my_bot, sb, a.timeout_ns)) {
+          atomicExch(a.error, 2u);
+          __trap();
+        }
+        a.seen[0] = st, a.seen[1] = sb;
+        __threadfence();
+      }
     }
   }
 }
@@ -140,8 +153,16 @@ cudaError_t launch_halo_push(const HaloPushArgs& a, int sms, cudaStream_t st) {
   const long long elems = (long long)(a.rows_first + a.rows_last) * (a.vec ? a.width / 4 : a.width);
   const long long want = (elems + 255) / 256;
   const int blocks = int(std::max<long long>(1, std::min<long long>(want, 2ll * sms)));
-  halo_push_kernel<<<blocks, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(blocks));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, halo_push_kernel, a);
 }
 
 cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag, unsigned* seen, unsigned* error,

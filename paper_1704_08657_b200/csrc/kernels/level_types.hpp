@@ -153,6 +153,14 @@ struct HaloPushArgs {
   const unsigned* pyramids;
   unsigned* error;
   unsigned long long timeout_ns;
+  // wait_after: the CTA that signals also waits for this rank's own halo
+  // arrivals (my_top / my_bot counters past seen[0] / seen[1]) before the
+  // kernel ends: push + wait in one launch (small levels, no interior split)
+  int wait_after;
+  const unsigned* my_top;
+  const unsigned* my_bot;
+  unsigned* seen;
+  int pdl;               // host only: launch with programmatic dependent launch
 };
 cudaError_t launch_halo_push(const HaloPushArgs& a, int sms, cudaStream_t st);
 cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag, unsigned* seen, unsigned* error,

@@ -967,7 +967,7 @@ StepIO step_input(const dwt2d_shard& s, size_t e, const float* strip, size_t pit
   return {ll_slot(s.ws, s.W, s.H, l), size_t(s.W >> l)};
 }
 
-void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, cudaStream_t st) {
+void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, bool wait_after, cudaStream_t st) {
   const ExchangeStep& x = s.steps[e];
   gpu::HaloPushArgs a{};
   a.src = io.cur, a.src_pitch = (long long)io.cur_pitch;
@@ -985,6 +985,11 @@ void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, cudaStream_t st) {
   a.pyramids = s.word(s.window, kPyramids);
   a.error = s.word(s.window, kError);
   a.timeout_ns = kExchangeTimeoutNs;
+  a.wait_after = wait_after ? 1 : 0;
+  a.my_top = s.word(s.window, kTopArrivals);
+  a.my_bot = s.word(s.window, kBotArrivals);
+  a.seen = s.word(s.window, kSeen);
+  a.pdl = s.plan->tune.pdl ? 1 : 0;
   cuda_check(gpu::launch_halo_push(a, sm_count(), st), "halo push launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1021,14 +1026,29 @@ void step_interior(const dwt2d_shard& s, const ExchangeStep& x, int& lo, int& hi
   if (hi - lo < 16) lo = hi = 0;
 }
 
-// part: 0 interior rows, 1 border rows (all rows when there is no interior)
+// Whether step e runs its interior rows while the halo rows travel (push,
+// interior, wait, border: four launches and more) or as push-and-wait in
+// one launch followed by the whole level (two launches). Splitting pays only
+// where the level itself takes long against the few microseconds of launch
+// latency each extra launch adds: level inputs of at least 64 MiB.
+bool split_step(const dwt2d_shard& s, size_t e) {
+  const ExchangeStep& x = s.steps[e];
+  int lo, hi, rows;
+  step_interior(s, x, lo, hi, rows);
+  return hi > lo && size_t(x.width) * size_t(x.height) * 4 >= (size_t(64) << 20);
+}
+
+// part: 0 interior rows, 1 border rows (all rows when there is no
+// interior), 2 all rows
 void shard_compute(dwt2d_shard& s, size_t e, const StepIO& io, float* out, size_t op, int part, cudaStream_t st) {
   const dwt2d_plan& p = *s.plan;
   const ExchangeStep& x = s.steps[e];
   int lo, hi, rows;
   step_interior(s, x, lo, hi, rows);
   std::vector<std::pair<int, int>> ranges;
-  if (part == 0) {
+  if (part == 2) {
+    ranges.push_back({0, rows});
+  } else if (part == 0) {
     if (hi > lo) ranges.push_back({lo, hi});
   } else if (hi > lo) {
     if (lo > 0) ranges.push_back({0, lo});
@@ -1779,13 +1799,14 @@ int dwt2d_shard_forward_mallat_ex(dwt2d_shard* s, const float* strip, size_t pit
     for (size_t e = 0; e < s->steps.size(); ++e) {
       void* const* ev = events ? events + 1 + 4 * e : nullptr;
       const StepIO io = step_input(*s, e, strip, pitch, out, out_pitch);
-      shard_push(*s, e, io, st);
+      const bool split = split_step(*s, e);
+      shard_push(*s, e, io, !split, st);
       if (ev) record(ev[0], st);
-      shard_compute(*s, e, io, out, out_pitch, 0, st);
+      if (split) shard_compute(*s, e, io, out, out_pitch, 0, st);
       if (ev) record(ev[1], st);
-      shard_wait(*s, st);
+      if (split) shard_wait(*s, st);
       if (ev) record(ev[2], st);
-      shard_compute(*s, e, io, out, out_pitch, 1, st);
+      shard_compute(*s, e, io, out, out_pitch, split ? 1 : 2, st);
       if (ev) record(ev[3], st);
     }
     shard_done(*s, st);
@@ -1869,18 +1890,26 @@ int dwt2d_forward_mallat_sharded(const dwt2d_plan* p, int nranks, const int* dev
     for (size_t e = 0; e < sh[0]->steps.size(); ++e) {
       std::vector<StepIO> io;
       for (int r = 0; r < nranks; ++r) io.push_back(step_input(*sh[r], e, strips[r], pitch[r], out[r], out_pitch[r]));
+      // push-and-wait in one launch is only safe phase-major when the ranks
+      // run on distinct streams; ranks sharing a stream always split
+      bool shared = false;
+      for (int r = 0; r < nranks && !shared; ++r)
+        for (int q = 0; q < r && !shared; ++q) shared = st(q) == st(r) && sh[q]->device == sh[r]->device;
+      const bool split = shared || split_step(*sh[0], e);
       for (int r = 0; r < nranks; ++r) {
         DeviceGuard g(sh[r]->device);
-        shard_push(*sh[r], e, io[r], st(r));
+        shard_push(*sh[r], e, io[r], !split, st(r));
+      }
+      if (split) {
+        for (int r = 0; r < nranks; ++r) {
+          DeviceGuard g(sh[r]->device);
+          shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], 0, st(r));
+        }
       }
       for (int r = 0; r < nranks; ++r) {
         DeviceGuard g(sh[r]->device);
-        shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], 0, st(r));
-      }
-      for (int r = 0; r < nranks; ++r) {
-        DeviceGuard g(sh[r]->device);
-        shard_wait(*sh[r], st(r));
-        shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], 1, st(r));
+        if (split) shard_wait(*sh[r], st(r));
+        shard_compute(*sh[r], e, io[r], out[r], out_pitch[r], split ? 1 : 2, st(r));
       }
     }
     for (int r = 0; r < nranks; ++r) {
