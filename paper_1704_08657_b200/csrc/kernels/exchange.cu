@@ -103,11 +103,12 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
       (first ? a.dst_prev : a.dst_next)[dr * a.dst_pitch + c] = __ldcg(a.src + sr * a.src_pitch + c);
     }
   }
-  // last CTA out signals both neighbours: every thread's peer stores are
-  // made visible system-wide before its CTA arrives
-  __threadfence_system();
+  // last CTA out signals both neighbours. The CTA barrier orders every
+  // thread's peer stores before thread 0's system-scope fence, which is
+  // cumulative: they are visible system-wide before the CTA arrives
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     const unsigned prev = atomicAdd(a.arrive, 1u);
     if (prev == gridDim.x - 1) {
       *a.arrive = 0;  // ready for the next push (no other CTA touches it now)
