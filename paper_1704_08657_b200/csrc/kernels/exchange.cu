@@ -62,9 +62,12 @@ __device__ bool spin_until(const unsigned* flag, unsigned target, unsigned long 
 
 __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ HaloPushArgs a) {
   // PDL: resident during the previous level's tail; its LL rows (this
-  // push's source) are complete after the wait
+  // push's source) are complete after the wait. A push that also waits for
+  // the neighbours' rows never releases its dependents early: their CTAs
+  // would sit resident at their own griddepcontrol.wait, and ranks sharing
+  // a GPU (virtual ranks) could then starve the neighbour's push of SMs.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" :::);
+  if (!a.wait_after) asm volatile("griddepcontrol.launch_dependents;" :::);
   if (a.first_step) {
     // the neighbours must have finished the previous pyramid (stopped
     // reading the halo buffers this push overwrites)

@@ -39,12 +39,14 @@ for L in range(1, a.max_levels + 1):
     with torch.cuda.graph(g, stream=st):
         for _ in range(a.iters):
             plan.forward_mallat(img, L, out=out, scratch=scratch, stream=st.cuda_stream)
-    g.replay()
+    with torch.cuda.stream(st):
+        g.replay()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(st)
-    g.replay()
-    t1.record(st)
+    with torch.cuda.stream(st):
+        t0.record(st)
+        g.replay()
+        t1.record(st)
     t1.synchronize()
     us = t0.elapsed_time(t1) / a.iters * 1e3
     print(f"levels {L}: {us:8.1f} us per pyramid  (+{us - prev:6.1f})", flush=True)

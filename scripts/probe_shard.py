@@ -53,12 +53,14 @@ with torch.cuda.graph(g, stream=st):
         for sh, s, o in zip(shards, strips, outs):
             sh.forward_mallat(s, out=o, stream=st) if a.world == 1 else None
 if a.world == 1:
-    g.replay()
+    with torch.cuda.stream(st):
+        g.replay()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record(st)
-    g.replay()
-    t1.record(st)
+    with torch.cuda.stream(st):
+        t0.record(st)
+        g.replay()
+        t1.record(st)
     t1.synchronize()
     print(f"graph: {t0.elapsed_time(t1) / a.iters * 1e3:.1f} us per pyramid; "
           f"single-GPU forward_mallat for comparison below")
@@ -67,10 +69,12 @@ if a.world == 1:
     with torch.cuda.graph(g2, stream=st):
         for _ in range(a.iters):
             plan.forward_mallat(img, a.levels, out=full, stream=st.cuda_stream)
-    g2.replay()
+    with torch.cuda.stream(st):
+        g2.replay()
     torch.cuda.synchronize()
-    t0.record(st)
-    g2.replay()
-    t1.record(st)
+    with torch.cuda.stream(st):
+        t0.record(st)
+        g2.replay()
+        t1.record(st)
     t1.synchronize()
     print(f"graph: {t0.elapsed_time(t1) / a.iters * 1e3:.1f} us per single-GPU pyramid")
