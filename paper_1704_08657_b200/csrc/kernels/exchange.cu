@@ -62,12 +62,11 @@ __device__ bool spin_until(const unsigned* flag, unsigned target, unsigned long 
 
 __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ HaloPushArgs a) {
   // PDL: resident during the previous level's tail; its LL rows (this
-  // push's source) are complete after the wait. A push that also waits for
-  // the neighbours' rows never releases its dependents early: their CTAs
-  // would sit resident at their own griddepcontrol.wait, and ranks sharing
-  // a GPU (virtual ranks) could then starve the neighbour's push of SMs.
+  // push's source) are complete after the wait. Dependents are released
+  // early only after every wait on another rank: a dependent's CTAs sit
+  // resident at their own griddepcontrol.wait, and on ranks sharing a GPU
+  // (virtual ranks) they could starve the neighbour that is being waited for.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (!a.wait_after) asm volatile("griddepcontrol.launch_dependents;" :::);
   if (a.first_step) {
     // the neighbours must have finished the previous pyramid (stopped
     // reading the halo buffers this push overwrites)
@@ -80,6 +79,9 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
     __syncthreads();
     if (!ok) __trap();
   }
+  // dependents (the interior rows) may become resident only once this CTA
+  // is past every wait on other ranks (see above)
+  if (!a.wait_after) asm volatile("griddepcontrol.launch_dependents;" :::);
   // rows [0, rows_first) -> dst_prev, rows [height - rows_last, height) -> dst_next
   const int rows = a.rows_first + a.rows_last;
   if (a.vec) {
