@@ -19,8 +19,8 @@
 // All counters are monotonic and live in device memory, so the sequence is
 // stream-ordered and can be captured in a CUDA graph and replayed: no host
 // round trip per level. A wait that does not complete within the timeout
-// records an error word and traps (a mis-connected ring fails loudly instead
-// of hanging the GPU).
+// records what it waited for in host-mapped memory and traps (a broken ring
+// fails loudly instead of hanging the GPU; dwt2d_shard_status reports it).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -60,6 +60,18 @@ __device__ bool spin_until(const unsigned* flag, unsigned target, unsigned long 
   return true;
 }
 
+// A wait that timed out: what it waited for goes to the shard's
+// diagnostics block in host-mapped memory (readable by the host after the
+// trap has taken the context down): code, the counter's value, the target.
+__device__ void report_and_trap(unsigned* diag, unsigned code, const unsigned* flag, unsigned target) {
+  volatile unsigned* d = diag;
+  d[1] = ld_acquire_sys(flag);
+  d[2] = target;
+  d[0] = code;
+  __threadfence_system();
+  __trap();
+}
+
 __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ HaloPushArgs a) {
   // PDL: resident during the previous level's tail; its LL rows (this
   // push's source) are complete after the wait. Dependents are released
@@ -70,14 +82,11 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
   if (a.first_step) {
     // the neighbours must have finished the previous pyramid (stopped
     // reading the halo buffers this push overwrites)
-    __shared__ int ok;
     if (threadIdx.x == 0) {
       const unsigned target = 2u * *a.pyramids;
-      ok = spin_until(a.done, target, a.timeout_ns);
-      if (!ok) atomicExch(a.error, 1u);
+      if (!spin_until(a.done, target, a.timeout_ns)) report_and_trap(a.error, 1u, a.done, target);
     }
     __syncthreads();
-    if (!ok) __trap();
   }
   // dependents (the interior rows) may become resident only once this CTA
   // is past every wait on other ranks (see above)
@@ -122,10 +131,8 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
       red_release_sys(a.flag_prev, 1u);
       if (a.wait_after) {
         const unsigned st = a.seen[0] + 1u, sb = a.seen[1] + 1u;
-        if (!spin_until(a.my_top, st, a.timeout_ns) || !spin_until(a.my_bot, sb, a.timeout_ns)) {
-          atomicExch(a.error, 2u);
-          __trap();
-        }
+        if (!spin_until(a.my_top, st, a.timeout_ns)) report_and_trap(a.error, 2u, a.my_top, st);
+        if (!spin_until(a.my_bot, sb, a.timeout_ns)) report_and_trap(a.error, 3u, a.my_bot, sb);
         a.seen[0] = st, a.seen[1] = sb;
         __threadfence();
       }
@@ -137,10 +144,8 @@ __global__ void halo_wait_kernel(const unsigned* top_flag, const unsigned* bot_f
                                  unsigned long long timeout_ns) {
   if (threadIdx.x != 0) return;
   const unsigned st = seen[0] + 1u, sb = seen[1] + 1u;
-  if (!spin_until(top_flag, st, timeout_ns) || !spin_until(bot_flag, sb, timeout_ns)) {
-    atomicExch(error, 2u);
-    __trap();
-  }
+  if (!spin_until(top_flag, st, timeout_ns)) report_and_trap(error, 2u, top_flag, st);
+  if (!spin_until(bot_flag, sb, timeout_ns)) report_and_trap(error, 3u, bot_flag, sb);
   seen[0] = st, seen[1] = sb;
   __threadfence();
 }
@@ -180,6 +185,16 @@ cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag,
 cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsigned* pyramids, cudaStream_t st) {
   pyramid_done_kernel<<<1, 32, 0, st>>>(done_prev, done_next, pyramids);
   return cudaGetLastError();
+}
+
+cudaError_t preload_exchange() {
+  cudaFuncAttributes fa;
+  for (const void* f : {reinterpret_cast<const void*>(halo_push_kernel), reinterpret_cast<const void*>(halo_wait_kernel),
+                        reinterpret_cast<const void*>(pyramid_done_kernel)}) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace gpu

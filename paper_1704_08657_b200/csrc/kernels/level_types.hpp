@@ -83,6 +83,10 @@ struct PlanEntry {
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
   PairLaunch pair;             // levels 1+2 in one pass (forward plans with reach <= 2, CW 4)
   LevelOccupancy pair_occupancy;
+  // loads every kernel of the entry into the context now (lazy module
+  // loading would otherwise load at first launch, which waits for running
+  // kernels: a deadlock when one of them spins on work not yet launched)
+  cudaError_t (*preload)();
 };
 
 // One sub-step of the generic executor (kernels/generic_step.cu). `taps`
@@ -151,7 +155,7 @@ struct HaloPushArgs {
   int first_step;        // first push of a pyramid: wait for *done >= 2 * *pyramids
   const unsigned* done;
   const unsigned* pyramids;
-  unsigned* error;
+  unsigned* error;       // diagnostics block (host-mapped): code, counter value, target
   unsigned long long timeout_ns;
   // wait_after: the CTA that signals also waits for this rank's own halo
   // arrivals (my_top / my_bot counters past seen[0] / seen[1]) before the
@@ -166,6 +170,7 @@ cudaError_t launch_halo_push(const HaloPushArgs& a, int sms, cudaStream_t st);
 cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag, unsigned* seen, unsigned* error,
                              unsigned long long timeout_ns, cudaStream_t st);
 cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsigned* pyramids, cudaStream_t st);
+cudaError_t preload_exchange();
 
 const std::vector<PlanEntry>& plan_registry();
 const PlanEntry* find_plan(unsigned long long fingerprint);

@@ -111,6 +111,28 @@ int pair_occupancy() {
 }
 
 template <class P, bool kForward>
+cudaError_t preload_entry() {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaSuccess;
+  auto load = [&](const void* f) {
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f);
+  };
+  load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, false, true>));
+  load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, false, false>));
+  if constexpr (kForward) {
+    load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, true>));
+    load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, false>));
+    load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, true, true>));
+    if constexpr (PairTraits<P>::ok && P::kAlt) load(reinterpret_cast<const void*>(pair_kernel<P>));
+  } else {
+    load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, true, true>));
+    load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, true, false>));
+    if constexpr (P::kCW == 4) load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, true, true, true>));
+  }
+  return e;
+}
+
+template <class P, bool kForward>
 PlanEntry make_entry() {
   using M = Meta<P>;
   PlanEntry e{};
@@ -121,6 +143,7 @@ PlanEntry make_entry() {
   e.up = M::U, e.down = M::L, e.left = M::HL, e.right = M::HR;
   e.taps_per_quad = P::kTaps;
   e.planar = &launch_level<P, false, false>;
+  e.preload = &preload_entry<P, kForward>;
   if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;
     e.occupancy = &level_occupancy<P, true, false>;

@@ -859,8 +859,7 @@ void forward_mallat_strip(const dwt2d_plan& p, const float* strip, size_t pitch,
 // single member: the pushes wrap the strip onto itself (periodic image).
 
 // window header: counters on separate 128-byte lines (unsigned words)
-constexpr int kTopArrivals = 0, kBotArrivals = 32, kDone = 64, kSeen = 96, kArrive = 128, kPyramids = 160,
-              kError = 192;
+constexpr int kTopArrivals = 0, kBotArrivals = 32, kDone = 64, kSeen = 96, kArrive = 128, kPyramids = 160;
 constexpr size_t kHeaderBytes = 1024;
 constexpr unsigned long long kExchangeTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s: a broken ring traps
 
@@ -888,6 +887,10 @@ struct dwt2d_shard {
   char* next_win = nullptr;
   char* ipc_open[2] = {nullptr, nullptr};  // handles opened with cudaIpcOpenMemHandle
   bool connected = false;
+  // diagnostics of a wait that timed out (host-mapped: readable after the
+  // trap took the context down): code, counter value, target
+  unsigned* diag_host = nullptr;
+  unsigned* diag_dev = nullptr;
   unsigned* word(char* win, int w) const { return reinterpret_cast<unsigned*>(win) + w; }
   ~dwt2d_shard() {
     int cur = 0;
@@ -897,6 +900,7 @@ struct dwt2d_shard {
       if (p) cudaIpcCloseMemHandle(p);
     if (window) cudaFree(window);
     if (ws) cudaFree(ws);
+    if (diag_host) cudaFreeHost(diag_host);
     cudaSetDevice(cur);
     cudaGetLastError();
   }
@@ -983,7 +987,7 @@ void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, bool wait_after, cud
   a.first_step = e == 0 ? 1 : 0;
   a.done = s.word(s.window, kDone);
   a.pyramids = s.word(s.window, kPyramids);
-  a.error = s.word(s.window, kError);
+  a.error = s.diag_dev;
   a.timeout_ns = kExchangeTimeoutNs;
   a.wait_after = wait_after ? 1 : 0;
   a.my_top = s.word(s.window, kTopArrivals);
@@ -996,7 +1000,7 @@ void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, bool wait_after, cud
 
 void shard_wait(dwt2d_shard& s, cudaStream_t st) {
   cuda_check(gpu::launch_halo_wait(s.word(s.window, kTopArrivals), s.word(s.window, kBotArrivals),
-                                   s.word(s.window, kSeen), s.word(s.window, kError), kExchangeTimeoutNs, st),
+                                   s.word(s.window, kSeen), s.diag_dev, kExchangeTimeoutNs, st),
              "halo wait launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1709,6 +1713,12 @@ int dwt2d_shard_create(const dwt2d_plan* p, int width, int strip_height, int lev
       fail(DWT2D_EUNSUPPORTED, "sharded pyramid: needs a fused kernel and periodic extension");
     if (world < 1 || rank < 0 || rank >= world) fail(DWT2D_EINVAL, "shard: rank outside [0, world)");
     check_pyramid(width, strip_height, levels);
+    // every kernel the shard launches is loaded now: a kernel loaded lazily
+    // at its first launch waits for the running kernels, and a halo wait
+    // spinning on a rank whose work this thread has not launched yet would
+    // never finish
+    cuda_check(gpu::preload_exchange(), "exchange kernels");
+    if (p->entry->preload) cuda_check(p->entry->preload(), "level kernels");
     auto sh = std::make_unique<dwt2d_shard>();
     sh->plan = p;
     sh->device = current_device();
@@ -1724,6 +1734,13 @@ int dwt2d_shard_create(const dwt2d_plan* p, int width, int strip_height, int lev
       cuda_check(cudaMalloc(&w, ws), "shard workspace allocation");
       sh->ws = static_cast<float*>(w);
     }
+    void* dh = nullptr;
+    cuda_check(cudaHostAlloc(&dh, 64, cudaHostAllocMapped | cudaHostAllocPortable), "shard diagnostics");
+    sh->diag_host = static_cast<unsigned*>(dh);
+    std::memset(sh->diag_host, 0, 64);
+    void* dd = nullptr;
+    cuda_check(cudaHostGetDevicePointer(&dd, dh, 0), "shard diagnostics");
+    sh->diag_dev = static_cast<unsigned*>(dd);
     cuda_check(cudaDeviceSynchronize(), "exchange window init");
     if (world == 1) {  // the ring of one: pushes wrap the strip onto itself
       sh->prev = sh->next = sh.get();
@@ -1834,12 +1851,16 @@ int dwt2d_shard_info(const dwt2d_shard* s, int* steps, int* pair, size_t* halo_b
 int dwt2d_shard_status(const dwt2d_shard* s, int* error) {
   return guard([&] {
     if (!s || !error) fail(DWT2D_EINVAL, "null argument");
-    DeviceGuard g(s->device);
-    unsigned v = 0;
-    cuda_check(cudaMemcpy(&v, reinterpret_cast<const unsigned*>(s->window) + kError, sizeof v,
-                          cudaMemcpyDeviceToHost),
-               "read exchange status");
-    *error = int(v);
+    // host-mapped: no CUDA call, so it also answers after a trap
+    const volatile unsigned* d = s->diag_host;
+    *error = int(d[0]);
+    if (d[0]) {
+      static const char* const what[] = {"", "a neighbour never finished the previous pyramid",
+                                         "the rows from the previous rank never arrived",
+                                         "the rows from the next rank never arrived"};
+      g_error = std::string("sharded pyramid rank ") + std::to_string(s->rank) + ": " + what[d[0] & 3] +
+                " (counter " + std::to_string(d[1]) + ", waited for " + std::to_string(d[2]) + ")";
+    }
   });
 }
 

@@ -270,12 +270,17 @@ class Shard:
         return {"steps": steps.value, "pair": bool(pair.value), "halo_bytes": hb.value}
 
     def status(self) -> int:
-        """0, or the exchange's error word (1: a neighbour never finished
-        the previous pyramid, 2: a halo never arrived)."""
+        """0, or the code of a halo wait that timed out (1: a neighbour never
+        finished the previous pyramid, 2 / 3: the rows from the previous /
+        next rank never arrived); readable after the trap (host memory).
+        status_message() describes it."""
         import ctypes
         v = ctypes.c_int()
         self._N.check(self._N.lib.dwt2d_shard_status(self._h, ctypes.byref(v)))
         return v.value
+
+    def status_message(self) -> str:
+        return self._N.lib.dwt2d_last_error().decode() if self.status() else ""
 
 
 def connect_ring(shards: Sequence["Shard"]) -> None:

@@ -36,12 +36,22 @@ nsteps = shards[0].info()["steps"]
 for _ in range(3):
     for sh, s, o, st in zip(shards, strips, outs, streams):
         sh.forward_mallat(s, out=o, stream=st)
-torch.cuda.synchronize()
+try:
+    torch.cuda.synchronize()
+except Exception:
+    for sh in shards:
+        print("rank", sh.rank, sh.status(), sh.status_message())
+    raise
 evs = [[Event() for _ in range(1 + 4 * nsteps)] for _ in range(a.iters)]
 for k in range(a.iters):
     for r, (sh, s, o, st) in enumerate(zip(shards, strips, outs, streams)):
         sh.forward_mallat(s, out=o, stream=st, events=evs[k] if r == 0 else None)
-torch.cuda.synchronize()
+try:
+    torch.cuda.synchronize()
+except Exception:
+    for sh in shards:
+        print("rank", sh.rank, sh.status(), sh.status_message())
+    raise
 for e in range(nsteps):
     b = 1 + 4 * e
     ph = [statistics.mean(x[i].elapsed_ms(x[i + 1]) for x in evs) * 1e3 for i in (b - 1, b, b + 1, b + 2)]

@@ -81,6 +81,35 @@ def test_sharded_per_rank_calls_on_separate_streams(cuda):
     assert all(sh.status() == 0 for sh in shards)
 
 
+def _fresh_process_per_rank(q):
+    import paper_1704_08657_b200 as dwt
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
+    W, Hs, world, L = 2048, 1024, 2, 8
+    img, strips = _full_and_strips(W, Hs, world, 13)
+    shards = [S.Shard(plan, W, Hs, L, r, world) for r in range(world)]
+    S.connect_ring(shards)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    outs = [sh.forward_mallat(s, stream=st) for sh, s, st in zip(shards, strips, streams)]
+    torch.cuda.synchronize()
+    full = plan.forward_mallat(img, L)
+    q.put(bool(torch.equal(S.assemble_mallat(outs, L), full.cpu())))
+
+
+def test_sharded_per_rank_calls_in_fresh_process():
+    """Rank after rank from one thread in a process that has launched none
+    of the level kernels yet: every kernel must already be loaded when the
+    first rank's halo wait spins (lazy loading at a later launch would wait
+    for it: a deadlock)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_fresh_process_per_rank, args=(q,))
+    p.start()
+    p.join(120)
+    assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
 def test_sharded_graph_capture_and_replay(cuda):
     """The strip pyramids (pushes, waits and levels) captured in one CUDA
     graph replay correctly (the counters live on the device)."""
