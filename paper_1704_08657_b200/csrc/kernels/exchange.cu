@@ -13,8 +13,9 @@
 //   halo_wait_kernel    one thread spins (acquire, system scope) until both
 //                       of my arrival counters passed the count it has seen
 //   pyramid_done_kernel after a rank's last level: tells both neighbours it
-//                       no longer reads its halo buffers; the next pyramid's
-//                       first push waits for that before overwriting them
+//                       no longer reads its halo buffers
+//   pyramid_start_kernel before the next pyramid's first push: waits for
+//                       both neighbours' done signals
 //
 // All counters are monotonic and live in device memory, so the sequence is
 // stream-ordered and can be captured in a CUDA graph and replayed: no host
@@ -74,22 +75,12 @@ __device__ void report_and_trap(unsigned* diag, unsigned code, const unsigned* f
 
 __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ HaloPushArgs a) {
   // PDL: resident during the previous level's tail; its LL rows (this
-  // push's source) are complete after the wait. Dependents are released
-  // early only after every wait on another rank: a dependent's CTAs sit
-  // resident at their own griddepcontrol.wait, and on ranks sharing a GPU
-  // (virtual ranks) they could starve the neighbour that is being waited for.
+  // push's source) are complete after the wait. A push that also waits for
+  // the neighbours (wait_after) releases no dependents early: their CTAs
+  // would sit resident at their own griddepcontrol.wait and, on ranks
+  // sharing a GPU (virtual ranks), could starve the neighbour being waited
+  // for. For the same reason every wait on another rank spins in ONE CTA.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.first_step) {
-    // the neighbours must have finished the previous pyramid (stopped
-    // reading the halo buffers this push overwrites)
-    if (threadIdx.x == 0) {
-      const unsigned target = 2u * *a.pyramids;
-      if (!spin_until(a.done, target, a.timeout_ns)) report_and_trap(a.error, 1u, a.done, target);
-    }
-    __syncthreads();
-  }
-  // dependents (the interior rows) may become resident only once this CTA
-  // is past every wait on other ranks (see above)
   if (!a.wait_after) asm volatile("griddepcontrol.launch_dependents;" :::);
   // rows [0, rows_first) -> dst_prev, rows [height - rows_last, height) -> dst_next
   const int rows = a.rows_first + a.rows_last;
@@ -150,6 +141,16 @@ __global__ void halo_wait_kernel(const unsigned* top_flag, const unsigned* bot_f
   __threadfence();
 }
 
+// Before a pyramid's first push: the neighbours must have finished the
+// previous pyramid (stopped reading the halo buffers the push overwrites).
+__global__ void pyramid_start_kernel(const unsigned* done, const unsigned* pyramids, unsigned* error,
+                                     unsigned long long timeout_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned target = 2u * *pyramids;
+  if (!spin_until(done, target, timeout_ns)) report_and_trap(error, 1u, done, target);
+  __threadfence();
+}
+
 __global__ void pyramid_done_kernel(unsigned* done_prev, unsigned* done_next, unsigned* pyramids) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
@@ -182,6 +183,12 @@ cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag,
   return cudaGetLastError();
 }
 
+cudaError_t launch_pyramid_start(const unsigned* done, const unsigned* pyramids, unsigned* error,
+                                 unsigned long long timeout_ns, cudaStream_t st) {
+  pyramid_start_kernel<<<1, 32, 0, st>>>(done, pyramids, error, timeout_ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsigned* pyramids, cudaStream_t st) {
   pyramid_done_kernel<<<1, 32, 0, st>>>(done_prev, done_next, pyramids);
   return cudaGetLastError();
@@ -190,7 +197,8 @@ cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsign
 cudaError_t preload_exchange() {
   cudaFuncAttributes fa;
   for (const void* f : {reinterpret_cast<const void*>(halo_push_kernel), reinterpret_cast<const void*>(halo_wait_kernel),
-                        reinterpret_cast<const void*>(pyramid_done_kernel)}) {
+                        reinterpret_cast<const void*>(pyramid_done_kernel),
+                        reinterpret_cast<const void*>(pyramid_start_kernel)}) {
     const cudaError_t e = cudaFuncGetAttributes(&fa, f);
     if (e != cudaSuccess) return e;
   }

@@ -152,9 +152,6 @@ struct HaloPushArgs {
   unsigned* flag_prev;   // prev's bottom-halo arrival counter
   unsigned* flag_next;   // next's top-halo arrival counter
   unsigned* arrive;      // this rank's CTA arrival counter (last CTA signals)
-  int first_step;        // first push of a pyramid: wait for *done >= 2 * *pyramids
-  const unsigned* done;
-  const unsigned* pyramids;
   unsigned* error;       // diagnostics block (host-mapped): code, counter value, target
   unsigned long long timeout_ns;
   // wait_after: the CTA that signals also waits for this rank's own halo
@@ -170,6 +167,8 @@ cudaError_t launch_halo_push(const HaloPushArgs& a, int sms, cudaStream_t st);
 cudaError_t launch_halo_wait(const unsigned* top_flag, const unsigned* bot_flag, unsigned* seen, unsigned* error,
                              unsigned long long timeout_ns, cudaStream_t st);
 cudaError_t launch_pyramid_done(unsigned* done_prev, unsigned* done_next, unsigned* pyramids, cudaStream_t st);
+cudaError_t launch_pyramid_start(const unsigned* done, const unsigned* pyramids, unsigned* error,
+                                 unsigned long long timeout_ns, cudaStream_t st);
 cudaError_t preload_exchange();
 
 const std::vector<PlanEntry>& plan_registry();

@@ -984,9 +984,6 @@ void shard_push(dwt2d_shard& s, size_t e, const StepIO& io, bool wait_after, cud
   a.flag_prev = s.word(s.prev_win, kBotArrivals);
   a.flag_next = s.word(s.next_win, kTopArrivals);
   a.arrive = s.word(s.window, kArrive);
-  a.first_step = e == 0 ? 1 : 0;
-  a.done = s.word(s.window, kDone);
-  a.pyramids = s.word(s.window, kPyramids);
   a.error = s.diag_dev;
   a.timeout_ns = kExchangeTimeoutNs;
   a.wait_after = wait_after ? 1 : 0;
@@ -1002,6 +999,13 @@ void shard_wait(dwt2d_shard& s, cudaStream_t st) {
   cuda_check(gpu::launch_halo_wait(s.word(s.window, kTopArrivals), s.word(s.window, kBotArrivals),
                                    s.word(s.window, kSeen), s.diag_dev, kExchangeTimeoutNs, st),
              "halo wait launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void shard_start(dwt2d_shard& s, cudaStream_t st) {
+  cuda_check(gpu::launch_pyramid_start(s.word(s.window, kDone), s.word(s.window, kPyramids), s.diag_dev,
+                                       kExchangeTimeoutNs, st),
+             "pyramid start launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -1812,6 +1816,7 @@ int dwt2d_shard_forward_mallat_ex(dwt2d_shard* s, const float* strip, size_t pit
     check_shard_args(*s, strip, out);
     DeviceGuard g(s->device);
     const cudaStream_t st = as_stream(stream);
+    shard_start(*s, st);
     if (events) record(events[0], st);
     for (size_t e = 0; e < s->steps.size(); ++e) {
       void* const* ev = events ? events + 1 + 4 * e : nullptr;
@@ -1908,6 +1913,10 @@ int dwt2d_forward_mallat_sharded(const dwt2d_plan* p, int nranks, const int* dev
     auto st = [&](int r) { return streams ? as_stream(streams[r]) : cudaStream_t(nullptr); };
     // phase-major enqueue: every rank's push of a step before any rank's
     // wait, so ranks sharing a device (or a stream) cannot block each other
+    for (int r = 0; r < nranks; ++r) {
+      DeviceGuard g(sh[r]->device);
+      shard_start(*sh[r], st(r));
+    }
     for (size_t e = 0; e < sh[0]->steps.size(); ++e) {
       std::vector<StepIO> io;
       for (int r = 0; r < nranks; ++r) io.push_back(step_input(*sh[r], e, strips[r], pitch[r], out[r], out_pitch[r]));
