@@ -39,8 +39,8 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
-__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
-  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -117,9 +117,12 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const __grid_constant__ 
     const unsigned prev = atomicAdd(a.arrive, 1u);
     if (prev == gridDim.x - 1) {
       *a.arrive = 0;  // ready for the next push (no other CTA touches it now)
+      // every CTA fenced its stores before arriving; one more fence orders
+      // the count this CTA observed before the two signals (a release per
+      // signal would fence twice more: ~3-5 us each under peer traffic)
       __threadfence_system();
-      red_release_sys(a.flag_next, 1u);
-      red_release_sys(a.flag_prev, 1u);
+      red_relaxed_sys(a.flag_next, 1u);
+      red_relaxed_sys(a.flag_prev, 1u);
       if (a.wait_after) {
         const unsigned st = a.seen[0] + 1u, sb = a.seen[1] + 1u;
         if (!spin_until(a.my_top, st, a.timeout_ns)) report_and_trap(a.error, 2u, a.my_top, st);
@@ -154,8 +157,8 @@ __global__ void pyramid_start_kernel(const unsigned* done, const unsigned* pyram
 __global__ void pyramid_done_kernel(unsigned* done_prev, unsigned* done_next, unsigned* pyramids) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
-  red_release_sys(done_prev, 1u);
-  red_release_sys(done_next, 1u);
+  red_relaxed_sys(done_prev, 1u);
+  red_relaxed_sys(done_next, 1u);
   *pyramids += 1u;
 }
 
