@@ -149,10 +149,30 @@ struct Sched {
   }
 };
 
+// Packed FP32 (sm_100a FFMA2/FMUL2: two independent IEEE fma/mul per
+// instruction, each lane of the pair rounded exactly like the scalar op) for
+// the factored programs: a tap's weight is the same for every component
+// column of a lane, so columns go through the accumulation in pairs. VF:
+// 0 scalar, 1 pairs (c, c + 1), 2 pairs (c, c + CW/2). Composed programs keep
+// the scalar product-then-sum (the reference's rounding must not contract).
+#ifndef DWT2D_PACKED_FMA
+#define DWT2D_PACKED_FMA 1
+#endif
+constexpr int kPackedFma = DWT2D_PACKED_FMA;
+#ifndef DWT2D_LEVEL_PACKED_FMA
+#define DWT2D_LEVEL_PACKED_FMA 0
+#endif
+constexpr int kLevelPackedFma = DWT2D_LEVEL_PACKED_FMA;
+
+template <int VF, int CW>
+__host__ __device__ constexpr int pair_col(int p, int half) {
+  return VF == 1 ? 2 * p + half : p + half * (CW / 2);
+}
+
 // UPW: rows stream bottom-up (the newest window row is the topmost one), so
 // a tap at row offset dn is (dn - min_dn) rows older than the newest instead
 // of (max_dn - dn). Same taps, same order: identical results.
-template <class P, int PF, int s, int u, int D, int CW, bool UPW>
+template <class P, int PF, int s, int u, int D, int CW, bool UPW, int VF = kPackedFma>
 __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW]) {
   using SC = Sched<P, PF>;
   constexpr int nhi = UPW ? -Meta<P>::nlo(s) : Meta<P>::nhi(s);  // age of the dn = 0 row
@@ -169,6 +189,36 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
       });
     } else if constexpr (row.tb == row.te) {  // an all-zero matrix row
       sfor<0, CW>([&](auto C_) { ring[s + 1][dst][r][decltype(C_)::value] = 0.0f; });
+    } else if constexpr (VF != 0 && P::kFma && CW % 2 == 0) {
+      // the scalar branch below, two columns per instruction
+      float2 acc[CW / 2];
+      constexpr int tb = row.tb;
+      constexpr float sc = row.scale;
+      sfor<row.tb, row.te>([&](auto T_) {
+        constexpr int ti = decltype(T_)::value;
+        constexpr TapDesc t = P::taps[ti];
+        constexpr int k = SC::slot(s, u, nhi - dsign * t.dn), j = t.j, dm = t.dm;
+        constexpr float w = t.w;
+        constexpr bool first = ti == tb;
+        sfor<0, CW / 2>([&](auto Q_) {
+          constexpr int q = decltype(Q_)::value;
+          constexpr int ca = pair_col<VF, CW>(q, 0), cb = pair_col<VF, CW>(q, 1);
+          const float2 v = make_float2(fetch<ca + dm, CW>(ring[s][k][j]), fetch<cb + dm, CW>(ring[s][k][j]));
+          if constexpr (!first)
+            acc[q] = __ffma2_rn(make_float2(w, w), v, acc[q]);
+          else if constexpr (w == 1.0f)
+            acc[q] = v;
+          else
+            acc[q] = __fmul2_rn(make_float2(w, w), v);
+        });
+      });
+      sfor<0, CW / 2>([&](auto Q_) {
+        constexpr int q = decltype(Q_)::value;
+        constexpr int ca = pair_col<VF, CW>(q, 0), cb = pair_col<VF, CW>(q, 1);
+        const float2 o = sc == 1.0f ? acc[q] : __fmul2_rn(acc[q], make_float2(sc, sc));
+        ring[s + 1][dst][r][ca] = o.x;
+        ring[s + 1][dst][r][cb] = o.y;
+      });
     } else {
       // acc = 0 + w0*v0 + w1*v1 + ... in table order. Composed programs round
       // like the reference's `acc += f.w * src` (executor.hpp:183: product
@@ -677,7 +727,8 @@ struct LeanRowWriter {
 // One work item: warp `wid` streams its (strip, chunk) of the level, top-down
 // or (UPW) bottom-up. RD: row reader type (default: RowReader, register
 // prefetch; tuning harnesses substitute staged readers).
-template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool UPW, class RD = void>
+template <class P, int PF, bool IN_IL, bool OUT_IL, bool VEC, bool COH, bool UPW, class RD = void,
+          int VF = kLevelPackedFma>
 __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, const int chunk) {
   using M = Meta<P>;
   using SC = Sched<P, PF>;
@@ -735,10 +786,10 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
           });
         });
       }
-      eval_step<P, PF, 0, u, D, CW, UPW>(ring);
+      eval_step<P, PF, 0, u, D, CW, UPW, VF>(ring);
       // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
       if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW>(ring); });
+      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW, VF>(ring); });
       const int y = UPW ? yfirst - i : yfirst + i;
       if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
       wr.advance();

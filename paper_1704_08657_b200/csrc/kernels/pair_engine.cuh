@@ -35,7 +35,12 @@ struct PairTraits {
   static constexpr bool ok = P::kCW == 4 && M::HL <= 2 && M::HR <= 2;
 };
 
-template <class P>
+// VF: packed-FMA form of the sub-steps (level_engine.cuh: eval_step).
+// Level 2 runs on every odd LL_1 row, also before the first and after the
+// last row of the chunk (their outputs are never stored, and no stored
+// output reads them): the warp stays convergent, so the level-2 shuffles
+// need no collective re-convergence blocks.
+template <class P, int VF = kPackedFma>
 __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, const int chunk) {
   using M = Meta<P>;
   using SC = Sched<P, 1>;
@@ -101,9 +106,9 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
           });
         });
       }
-      eval_step<P, 1, 0, u, D, CW1, false>(ring1);
+      eval_step<P, 1, 0, u, D, CW1, false, VF>(ring1);
       if (i + 1 < rows1) rd.load(a1, ring1[0][SC::slot(0, u, -1)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW1, false>(ring1); });
+      sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW1, false, VF>(ring1); });
       constexpr int so = SC::slot(S, u, 0);
       const int y1 = yfirst1 + i;
       if (y1 >= 2 * m0 && y1 < 2 * m1 && st1) w1.store_from<1>(a1, ring1[S][so]);
@@ -119,8 +124,8 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
         });
       } else {
         constexpr int u2 = (((u - (U + L) - 1) / 2) % UNR1 + UNR1) % UNR1;
-        const int i2 = (k - 1) / 2;
-        if (k >= 1 && i2 < rows2) {
+        const int i2 = (k - 1) >> 1;  // floor: distinct rows also before the chunk
+        {
           if constexpr (!SC::kCirc) {
             sfor<1, S + 1>([&](auto B_) {
               constexpr int b = decltype(B_)::value;
@@ -144,10 +149,12 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
             ring2[0][s0][2][c] = ring1[S][so][0][2 * c];
             ring2[0][s0][3][c] = ring1[S][so][0][2 * c + 1];
           });
-          sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u2, D, CW2, false>(ring2); });
+          sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u2, D, CW2, false, VF>(ring2); });
           const int y2 = yfirst2 + i2;
-          if (y2 >= m0 && y2 < m1 && st2) w2.store_from<0>(a2, ring2[S][SC::slot(S, u2, 0)]);
-          w2.advance();
+          if (y2 >= m0 && y2 < m1 && st2) {
+            w2.y = y2;
+            w2.store_from<0>(a2, ring2[S][SC::slot(S, u2, 0)]);
+          }
         }
       }
     });
