@@ -149,12 +149,17 @@ struct Sched {
   }
 };
 
-// Packed FP32 (sm_100a FFMA2/FMUL2: two independent IEEE fma/mul per
-// instruction, each lane of the pair rounded exactly like the scalar op) for
-// the factored programs: a tap's weight is the same for every component
-// column of a lane, so columns go through the accumulation in pairs. VF:
-// 0 scalar, 1 pairs (c, c + 1), 2 pairs (c, c + CW/2). Composed programs keep
-// the scalar product-then-sum (the reference's rounding must not contract).
+// Packed FP32 (sm_100a FFMA2/FADD2: two independent IEEE operations per
+// instruction, each half rounded exactly like the scalar op): a tap's weight
+// is the same for every component column of a lane, so columns go through
+// the accumulation in pairs. VF (factored programs): 0 scalar, 1 pairs
+// (c, c + 1), 2 pairs (c, c + CW/2). Composed programs (the reference's
+// product-then-sum rounding, executor.hpp:183) are packed with pairs
+// (c, c + 1) when kComposedPacked is set: ptxas contracts mul.rn.f32x2 +
+// add.rn.f32x2 into FFMA2 even with --fmad=false (checked with nvcc 12.9),
+// so every packed product is written fma(w, v, nz) with nz = -0.0f read from
+// the launch arguments (opaque to ptxas, and round(w*v + -0) == round(w*v)
+// for every w*v including signed zeros) and cannot be fused into the sum.
 #ifndef DWT2D_PACKED_FMA
 #define DWT2D_PACKED_FMA 1
 #endif
@@ -163,24 +168,216 @@ constexpr int kPackedFma = DWT2D_PACKED_FMA;
 #define DWT2D_LEVEL_PACKED_FMA 0
 #endif
 constexpr int kLevelPackedFma = DWT2D_LEVEL_PACKED_FMA;
+#ifndef DWT2D_COMPOSED_PACKED
+#define DWT2D_COMPOSED_PACKED 1
+#endif
+constexpr bool kComposedPacked = DWT2D_COMPOSED_PACKED != 0;
+
+// packed form of a composed program: the plan's kPack trait where it has one
+template <class P>
+constexpr bool composed_packed() {
+  if constexpr (requires { P::kPack; }) return P::kPack;
+  else return kComposedPacked;
+}
 
 template <int VF, int CW>
 __host__ __device__ constexpr int pair_col(int p, int half) {
   return VF == 1 ? 2 * p + half : p + half * (CW / 2);
 }
 
+// Evaluation order of one sub-step. Every output component's sum keeps its
+// table order (so the rounding is the reference's); when each arithmetic
+// row's taps are sorted by source (component j, row dn) — the composed
+// programs' are (executor.hpp:79-90) — the rows advance together, one
+// (j, dn) block at a time. A block first fetches the source row's columns
+// its taps read (the neighbour lanes' columns by one shuffle each: shuffles
+// are not merged by the compiler) and every tap of every output then reads
+// those registers; the next block's replace them, so a 256-tap composed
+// convolution keeps one source row's halo live instead of all of them.
+// Otherwise (factored programs): one block, rows in table order, every
+// source row's halo fetched once for the whole sub-step.
+template <class P, int s, int CW>
+struct StepOrder {
+  static constexpr int kMaxKeys = 64;
+  static constexpr int kCols = 3 * CW;  // columns -CW .. 2CW-1 (reach <= CW, Meta)
+  struct Data {
+    int nkeys = 0, nblocks = 0;
+    int kj[kMaxKeys] = {}, kdn[kMaxKeys] = {};
+    unsigned long long cols[kMaxKeys] = {};  // bit c + CW: column c of the key's row is read
+    int kb[kMaxKeys] = {}, ke[kMaxKeys] = {};  // keys of each block
+    int b[4][kMaxKeys] = {}, e[4][kMaxKeys] = {};  // taps of each row in each block
+  };
+  static constexpr int key(const TapDesc& t) { return t.j * 256 + t.dn + 128; }
+  static constexpr Data build() {
+    Data d{};
+    bool sorted = true;
+    int keys[kMaxKeys] = {};
+    int n = 0;
+    for (int r = 0; r < 4; ++r) {
+      const RowDesc row = P::rows[s * 4 + r];
+      if (row.ident) continue;
+      for (int t = row.tb; t < row.te; ++t) {
+        if (t > row.tb && key(P::taps[t]) < key(P::taps[t - 1])) sorted = false;
+        bool seen = false;
+        for (int q = 0; q < n; ++q) seen = seen || keys[q] == key(P::taps[t]);
+        if (!seen) keys[n++] = key(P::taps[t]);
+      }
+    }
+    for (int i = 0; i < n; ++i)  // sort the keys
+      for (int k = i + 1; k < n; ++k)
+        if (keys[k] < keys[i]) {
+          const int x = keys[i];
+          keys[i] = keys[k], keys[k] = x;
+        }
+    d.nkeys = n;
+    for (int q = 0; q < n; ++q) {
+      d.kj[q] = keys[q] / 256, d.kdn[q] = keys[q] % 256 - 128;
+      for (int r = 0; r < 4; ++r) {
+        const RowDesc row = P::rows[s * 4 + r];
+        if (row.ident) continue;
+        for (int t = row.tb; t < row.te; ++t)
+          for (int c = 0; c < CW; ++c)
+            if (key(P::taps[t]) == keys[q]) d.cols[q] |= 1ull << (c + P::taps[t].dm + CW);
+      }
+    }
+    if (!sorted || n == 0) {  // one block: all keys, rows in table order
+      d.nblocks = 1;
+      d.kb[0] = 0, d.ke[0] = n;
+      for (int r = 0; r < 4; ++r) {
+        const RowDesc row = P::rows[s * 4 + r];
+        d.b[r][0] = row.tb, d.e[r][0] = row.ident ? row.tb : row.te;
+      }
+      return d;
+    }
+    d.nblocks = n;
+    for (int q = 0; q < n; ++q) {
+      d.kb[q] = q, d.ke[q] = q + 1;
+      for (int r = 0; r < 4; ++r) {
+        const RowDesc row = P::rows[s * 4 + r];
+        int b = row.tb, e = row.tb;
+        bool any = false;
+        if (!row.ident)
+          for (int t = row.tb; t < row.te; ++t)
+            if (key(P::taps[t]) == keys[q]) {
+              if (!any) b = t;
+              any = true;
+              e = t + 1;
+            }
+        d.b[r][q] = b, d.e[r][q] = e;
+      }
+    }
+    return d;
+  }
+  static constexpr Data d = build();
+  // whether a packed tap reads the pair starting at column m (pairing pv)
+  static constexpr bool pair_needed(int q, int m, int pv) {
+    for (int r = 0; r < 4; ++r) {
+      const RowDesc row = P::rows[s * 4 + r];
+      if (row.ident) continue;
+      for (int t = row.tb; t < row.te; ++t)
+        if (key(P::taps[t]) == key_of(q))
+          for (int c = 0; c < CW / 2; ++c)
+            if ((pv == 1 ? 2 * c : c) + P::taps[t].dm == m) return true;
+    }
+    return false;
+  }
+  static constexpr int key_of(int q) { return d.kj[q] * 256 + d.kdn[q] + 128; }
+  static constexpr int index(int j, int dn) {
+    for (int q = 0; q < d.nkeys; ++q)
+      if (d.kj[q] == j && d.kdn[q] == dn) return q;
+    return -1;
+  }
+};
+
 // UPW: rows stream bottom-up (the newest window row is the topmost one), so
 // a tap at row offset dn is (dn - min_dn) rows older than the newest instead
 // of (max_dn - dn). Same taps, same order: identical results.
 template <class P, int PF, int s, int u, int D, int CW, bool UPW, int VF = kPackedFma>
-__device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW]) {
+__device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW], const float nz) {
   using SC = Sched<P, PF>;
+  using O = StepOrder<P, s, CW>;
   constexpr int nhi = UPW ? -Meta<P>::nlo(s) : Meta<P>::nhi(s);  // age of the dn = 0 row
   constexpr int dsign = UPW ? -1 : 1;
   constexpr int dst = SC::slot(s + 1, u, 0);
+  constexpr bool pack = CW % 2 == 0 && (P::kFma ? VF != 0 : composed_packed<P>());
+  constexpr int PV = P::kFma ? VF : 2;  // pairing of the packed form
+  constexpr int NA = pack ? CW / 2 : CW;
+  // acc = 0 + w0*v0 + w1*v1 + ... in table order. Composed programs round
+  // like the reference's `acc += f.w * src` (executor.hpp:183: product
+  // rounded, then the sum); factored programs fuse each tap into one fma.
+  // The first tap is a plain product (a copy when w0 == 1).
+  using Acc = std::conditional_t<pack, float2, float>;
+  Acc acc[4][NA];
+  const float2 nz2 = make_float2(nz, nz);
+  sfor<0, O::d.nblocks>([&](auto Q_) {
+    constexpr int q = decltype(Q_)::value;
+    // the block's source rows, halo columns included: ext[key][c + CW]; for
+    // the packed form also every operand pair the taps read, built once per
+    // block (ext2[key][m + CW] = columns m and m + pair_col(0, 1)): pairs
+    // assembled per tap cost a register move each
+    constexpr int NK = O::d.nkeys > 0 ? O::d.nkeys : 1;
+    constexpr int POFF = pair_col<PV, CW>(0, 1);
+    float ext[NK][O::kCols];
+    float2 ext2[pack ? NK : 1][O::kCols];
+    sfor<O::d.kb[q], O::d.ke[q]>([&](auto K_) {
+      constexpr int key = decltype(K_)::value;
+      constexpr int k = SC::slot(s, u, nhi - dsign * O::d.kdn[key]), j = O::d.kj[key];
+      sfor<0, O::kCols>([&](auto C_) {
+        constexpr int c = decltype(C_)::value - CW;
+        if constexpr ((O::d.cols[key] >> (c + CW)) & 1ull) ext[key][c + CW] = fetch<c, CW>(ring[s][k][j]);
+      });
+      if constexpr (pack) {
+        sfor<0, O::kCols>([&](auto C_) {
+          constexpr int m = decltype(C_)::value - CW;
+          if constexpr (O::pair_needed(key, m, PV)) ext2[key][m + CW] = make_float2(ext[key][m + CW], ext[key][m + POFF + CW]);
+        });
+      }
+    });
+    sfor<0, 4>([&](auto R_) {
+      constexpr int r = decltype(R_)::value;
+      constexpr int tb = P::rows[s * 4 + r].tb;
+      sfor<O::d.b[r][q], O::d.e[r][q]>([&](auto T_) {
+        constexpr int ti = decltype(T_)::value;
+        constexpr TapDesc t = P::taps[ti];
+        // scalar copies: nested lambdas may only use scalar constexpr locals
+        constexpr int key = O::index(t.j, t.dn), dm = t.dm;
+        constexpr float w = t.w;
+        constexpr bool first = ti == tb;
+        if constexpr (pack) {
+          sfor<0, NA>([&](auto C_) {
+            constexpr int c = decltype(C_)::value;
+            constexpr int ca = pair_col<PV, CW>(c, 0), cb = pair_col<PV, CW>(c, 1);
+            static_assert(cb - ca == POFF, "pair layout");
+            const float2 v = ext2[key][ca + dm + CW];
+            const float2 wv = w == 1.0f ? v : __ffma2_rn(make_float2(w, w), v, nz2);
+            if constexpr (first)
+              acc[r][c] = wv;
+            else if constexpr (P::kFma)
+              acc[r][c] = __ffma2_rn(make_float2(w, w), v, acc[r][c]);
+            else
+              acc[r][c] = __fadd2_rn(acc[r][c], wv);
+          });
+        } else {
+          sfor<0, CW>([&](auto C_) {
+            constexpr int c = decltype(C_)::value;
+            const float v = ext[key][c + dm + CW];
+            if constexpr (!first && P::kFma)
+              acc[r][c] = __fmaf_rn(w, v, acc[r][c]);
+            else if constexpr (!first)  // reference rounding: product, then sum
+              acc[r][c] = __fadd_rn(acc[r][c], w == 1.0f ? v : __fmul_rn(w, v));
+            else if constexpr (w == 1.0f)
+              acc[r][c] = v;
+            else
+              acc[r][c] = __fmul_rn(w, v);
+          });
+        }
+      });
+    });
+  });
   sfor<0, 4>([&](auto R_) {
     constexpr int r = decltype(R_)::value;
     constexpr RowDesc row = P::rows[s * 4 + r];
+    constexpr float sc = row.scale;
     if constexpr (row.ident) {
       constexpr int src = SC::slot(s, u, nhi);
       sfor<0, CW>([&](auto C_) {
@@ -189,70 +386,21 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
       });
     } else if constexpr (row.tb == row.te) {  // an all-zero matrix row
       sfor<0, CW>([&](auto C_) { ring[s + 1][dst][r][decltype(C_)::value] = 0.0f; });
-    } else if constexpr (VF != 0 && P::kFma && CW % 2 == 0) {
-      // the scalar branch below, two columns per instruction
-      float2 acc[CW / 2];
-      constexpr int tb = row.tb;
-      constexpr float sc = row.scale;
-      sfor<row.tb, row.te>([&](auto T_) {
-        constexpr int ti = decltype(T_)::value;
-        constexpr TapDesc t = P::taps[ti];
-        constexpr int k = SC::slot(s, u, nhi - dsign * t.dn), j = t.j, dm = t.dm;
-        constexpr float w = t.w;
-        constexpr bool first = ti == tb;
-        sfor<0, CW / 2>([&](auto Q_) {
-          constexpr int q = decltype(Q_)::value;
-          constexpr int ca = pair_col<VF, CW>(q, 0), cb = pair_col<VF, CW>(q, 1);
-          const float2 v = make_float2(fetch<ca + dm, CW>(ring[s][k][j]), fetch<cb + dm, CW>(ring[s][k][j]));
-          if constexpr (!first)
-            acc[q] = __ffma2_rn(make_float2(w, w), v, acc[q]);
-          else if constexpr (w == 1.0f)
-            acc[q] = v;
-          else
-            acc[q] = __fmul2_rn(make_float2(w, w), v);
-        });
-      });
-      sfor<0, CW / 2>([&](auto Q_) {
-        constexpr int q = decltype(Q_)::value;
-        constexpr int ca = pair_col<VF, CW>(q, 0), cb = pair_col<VF, CW>(q, 1);
-        const float2 o = sc == 1.0f ? acc[q] : __fmul2_rn(acc[q], make_float2(sc, sc));
+    } else if constexpr (pack) {
+      sfor<0, NA>([&](auto C_) {
+        constexpr int c = decltype(C_)::value;
+        constexpr int ca = pair_col<PV, CW>(c, 0), cb = pair_col<PV, CW>(c, 1);
+        const float2 o = sc == 1.0f ? acc[r][c] : __ffma2_rn(acc[r][c], make_float2(sc, sc), nz2);
         ring[s + 1][dst][r][ca] = o.x;
         ring[s + 1][dst][r][cb] = o.y;
       });
     } else {
-      // acc = 0 + w0*v0 + w1*v1 + ... in table order. Composed programs round
-      // like the reference's `acc += f.w * src` (executor.hpp:183: product
-      // rounded, then the sum); factored programs fuse each tap into one
-      // fma. The first tap is a plain product (a copy when w0 == 1).
-      float acc[CW];
-      constexpr int tb = row.tb;
-      constexpr float sc = row.scale;
-      sfor<row.tb, row.te>([&](auto T_) {
-        constexpr int ti = decltype(T_)::value;
-        constexpr TapDesc t = P::taps[ti];
-        // scalar copies: nested lambdas may only use scalar constexpr locals
-        constexpr int k = SC::slot(s, u, nhi - dsign * t.dn), j = t.j, dm = t.dm;
-        constexpr float w = t.w;
-        constexpr bool first = ti == tb;
-        sfor<0, CW>([&](auto C_) {
-          constexpr int c = decltype(C_)::value;
-          const float v = fetch<c + dm, CW>(ring[s][k][j]);
-          if constexpr (!first && P::kFma)
-            acc[c] = __fmaf_rn(w, v, acc[c]);
-          else if constexpr (!first)  // reference rounding: product, then sum
-            acc[c] = __fadd_rn(acc[c], w == 1.0f ? v : __fmul_rn(w, v));
-          else if constexpr (w == 1.0f)
-            acc[c] = v;
-          else
-            acc[c] = __fmul_rn(w, v);
-        });
-      });
       sfor<0, CW>([&](auto C_) {
         constexpr int c = decltype(C_)::value;
         if constexpr (sc == 1.0f)
-          ring[s + 1][dst][r][c] = acc[c];
+          ring[s + 1][dst][r][c] = acc[r][c];
         else
-          ring[s + 1][dst][r][c] = __fmul_rn(acc[c], sc);
+          ring[s + 1][dst][r][c] = __fmul_rn(acc[r][c], sc);
       });
     }
   });
@@ -786,10 +934,10 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
           });
         });
       }
-      eval_step<P, PF, 0, u, D, CW, UPW, VF>(ring);
+      eval_step<P, PF, 0, u, D, CW, UPW, VF>(ring, a.neg_zero);
       // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
       if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW, VF>(ring); });
+      sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW, VF>(ring, a.neg_zero); });
       const int y = UPW ? yfirst - i : yfirst + i;
       if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
       wr.advance();

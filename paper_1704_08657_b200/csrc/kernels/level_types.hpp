@@ -41,6 +41,7 @@ struct LevelArgs {
   int alternate;        // 1: odd chunks stream bottom-up (shared warm-up rows hit L2)
   int staged;           // 1: interleaved input rows staged in shared memory by TMA
   int pdl;              // host only: launch with programmatic dependent launch
+  float neg_zero;       // -0.0f (set by the host: an operand ptxas cannot fold, level_engine.cuh)
   // Row strips (multi-GPU): when halo != 0, component rows above the strip
   // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from
   // halo_bot (row y - h2) instead of wrapping periodically inside the strip.

@@ -106,9 +106,9 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
           });
         });
       }
-      eval_step<P, 1, 0, u, D, CW1, false, VF>(ring1);
+      eval_step<P, 1, 0, u, D, CW1, false, VF>(ring1, a1.neg_zero);
       if (i + 1 < rows1) rd.load(a1, ring1[0][SC::slot(0, u, -1)]);
-      sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW1, false, VF>(ring1); });
+      sfor<1, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u, D, CW1, false, VF>(ring1, a1.neg_zero); });
       constexpr int so = SC::slot(S, u, 0);
       const int y1 = yfirst1 + i;
       if (y1 >= 2 * m0 && y1 < 2 * m1 && st1) w1.store_from<1>(a1, ring1[S][so]);
@@ -149,7 +149,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
             ring2[0][s0][2][c] = ring1[S][so][0][2 * c];
             ring2[0][s0][3][c] = ring1[S][so][0][2 * c + 1];
           });
-          sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u2, D, CW2, false, VF>(ring2); });
+          sfor<0, S>([&](auto S_) { eval_step<P, 1, decltype(S_)::value, u2, D, CW2, false, VF>(ring2, a1.neg_zero); });
           const int y2 = yfirst2 + i2;
           if (y2 >= m0 && y2 < m1 && st2) {
             w2.y = y2;

@@ -211,6 +211,7 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   if (a.w2 <= 0 || a.h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
   a.alternate = p.tune.alternate == 0 ? 0 : p.tune.alternate == 2 ? 2 : 1;  // 2: also single-wave levels (tests)
   a.pdl = p.tune.pdl ? 1 : 0;
+  a.neg_zero = -0.0f;
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);

@@ -1,0 +1,98 @@
+// Tuning harness (development only): one forward level of the composed
+// (reference-rounding) CDF 9/7 programs in several forms — component
+// columns per lane (CW 2/4) x scalar / packed (FFMA2 + FADD2) arithmetic —
+// register-prefetch kernel, 16384^2 and 4096^2, bits compared per program.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -lineinfo
+//        --expt-relaxed-constexpr -I include scripts/tune_composed.cu -o build/tune_composed
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../paper_1704_08657_b200/csrc/generated/plans_gen.cuh"
+#include "../paper_1704_08657_b200/csrc/kernels/level_engine.cuh"
+
+using namespace dwt2d_b200::gpu;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+template <class B, int CW_, bool PACK>
+struct V : B {
+  static constexpr int kCW = CW_;
+  static constexpr bool kPack = PACK;
+};
+
+__global__ void fill(float* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = (float)((i * 2654435761ull) % 1000003ull) * 1e-6f;
+}
+
+int sms;
+template <class P>
+void run(const char* name, int W, float* img, float* out, std::vector<float>& ref, bool first) {
+  auto kern = level_kernel<P, 2, true, false, true>;
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0));
+  const size_t n = size_t(W) * W;
+  LevelArgs a{};
+  const int w2 = W / 2;
+  for (int j = 0; j < 4; ++j) a.in[j] = img, a.in_pitch[j] = W;
+  for (int j = 0; j < 4; ++j) a.out[j] = out + j * (n / 4), a.out_pitch[j] = w2;
+  a.w2 = w2, a.h2 = w2, a.vec = 1, a.neg_zero = -0.0f;
+  a.nstrips = (w2 + kOutLanes * P::kCW - 1) / (kOutLanes * P::kCW);
+  const long long resident = (long long)occ * kWarpsPerCta * sms;
+  const long long rows_total = (long long)w2 * a.nstrips;
+  const long long per_warp = (rows_total + resident - 1) / resident;
+  long long chunk = per_warp <= 48 ? std::max<long long>(2, per_warp) : (rows_total + 5 * resident - 1) / (5 * resident);
+  a.chunk_rows = int(std::min<long long>(chunk, w2));
+  a.nchunks = (w2 + a.chunk_rows - 1) / a.chunk_rows;
+  const unsigned blocks = unsigned((a.nstrips * a.nchunks + 3) / 4);
+  CK(cudaMemset(out, 0, n * 4));
+  kern<<<blocks, 128>>>(a);
+  CK(cudaDeviceSynchronize());
+  std::vector<float> got(n);
+  CK(cudaMemcpy(got.data(), out, n * 4, cudaMemcpyDeviceToHost));
+  long long bad = 0;
+  if (first) ref = got;
+  else for (size_t i = 0; i < n; ++i) bad += memcmp(&got[i], &ref[i], 4) != 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0), cudaEventCreate(&e1);
+  const int iters = 20;
+  cudaEventRecord(e0);
+  for (int i = 0; i < iters; ++i) kern<<<blocks, 128>>>(a);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= iters;
+  printf("%5d^2 %-22s regs %3d spill-free? %s occ %d  %9.2f us  mismatches %lld\n", W, name, fa.numRegs,
+         fa.localSizeBytes ? "no " : "yes", occ, ms * 1e3, bad);
+}
+
+int main() {
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  using namespace plans;
+  for (int W : {16384, 4096}) {
+    const size_t n = size_t(W) * W;
+    float *img, *out;
+    CK(cudaMalloc(&img, n * 4));
+    CK(cudaMalloc(&out, n * 4));
+    fill<<<1184, 256>>>(img, (long long)n);
+    std::vector<float> ref;
+    run<V<cdf97_separable_convolution_base, 2, false>>("sepconv CW2 scalar", W, img, out, ref, true);
+    run<V<cdf97_separable_convolution_base, 2, true>>("sepconv CW2 packed", W, img, out, ref, false);
+    run<V<cdf97_separable_convolution_base, 4, false>>("sepconv CW4 scalar", W, img, out, ref, false);
+    run<V<cdf97_separable_convolution_base, 4, true>>("sepconv CW4 packed", W, img, out, ref, false);
+    run<V<cdf97_nonseparable_polyconvolution_base, 4, false>>("polyconv CW4 scalar", W, img, out, ref, true);
+    run<V<cdf97_nonseparable_polyconvolution_base, 4, true>>("polyconv CW4 packed", W, img, out, ref, false);
+    run<V<cdf97_nonseparable_polyconvolution_base, 2, false>>("polyconv CW2 scalar", W, img, out, ref, false);
+    run<V<cdf97_nonseparable_polyconvolution_base, 2, true>>("polyconv CW2 packed", W, img, out, ref, false);
+    run<V<cdf97_nonseparable_lifting_base, 4, false>>("nslift CW4 scalar", W, img, out, ref, true);
+    run<V<cdf97_nonseparable_lifting_base, 4, true>>("nslift CW4 packed", W, img, out, ref, false);
+    run<V<cdf97_separable_lifting_base, 4, false>>("seplift CW4 scalar", W, img, out, ref, true);
+    run<V<cdf97_separable_lifting_base, 4, true>>("seplift CW4 packed", W, img, out, ref, false);
+    cudaFree(img), cudaFree(out);
+  }
+  return 0;
+}
