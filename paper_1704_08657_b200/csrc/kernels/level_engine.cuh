@@ -765,10 +765,10 @@ template <int CW, bool IL, bool VEC, bool UPW = false>
 struct RowWriter {
   float* p[4];
   long long pitch[4];
-  int xc, w2;
+  int xc, kx0, kx1;  // columns stored: [kx0, kx1) (the keep window, LevelArgs)
 
   __device__ __forceinline__ void init(const LevelArgs& a, int xc_, int first_row) {
-    xc = xc_, w2 = a.w2;
+    xc = xc_, kx0 = a.keep_x0, kx1 = a.keep_x1;
     sfor<0, 4>([&](auto J_) {
       constexpr int j = decltype(J_)::value;
       if constexpr (IL) {
@@ -790,8 +790,12 @@ struct RowWriter {
     }
   }
 
-  // whether this lane's columns are inside the image (fixed per lane)
-  __device__ __forceinline__ bool lane_in_range() const { return VEC ? xc + CW <= w2 : xc < w2; }
+  // whether this lane stores (fixed per lane): the vector path stores all CW
+  // columns or none (keep windows are lane-aligned there), the scalar path
+  // checks each column
+  __device__ __forceinline__ bool lane_in_range() const {
+    return VEC ? xc >= kx0 && xc + CW <= kx1 : xc + CW > kx0 && xc < kx1;
+  }
 
   // planar vector rows of the three detail bands only (the LL band of a
   // level that feeds the next level in the same pass is not written)
@@ -834,7 +838,7 @@ struct RowWriter {
     } else {
       sfor<0, CW>([&](auto C_) {
         constexpr int c = decltype(C_)::value;
-        if (xc + c < w2) {
+        if (xc + c >= kx0 && xc + c < kx1) {
           sfor<0, 4>([&](auto J_) {
             constexpr int j = decltype(J_)::value;
             if constexpr (IL)
@@ -892,6 +896,7 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   const int rows = (y1 - y0) + M::U + M::L;
   const int iters = (rows + UNR - 1) / UNR * UNR;
   bool out_lane = lane >= 1 && lane <= kOutLanes;
+  const int ys0 = max(y0, a.keep_y0), ys1 = min(y1, a.keep_y1);  // rows stored
 
   float ring[S + 1][D][4][CW];
   sfor<1, S + 1>([&](auto B_) {
@@ -939,7 +944,7 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
       if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
       sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW, VF>(ring, a.neg_zero); });
       const int y = UPW ? yfirst - i : yfirst + i;
-      if (y >= y0 && y < y1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
+      if (y >= ys0 && y < ys1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);
       wr.advance();
     });
   }

@@ -41,6 +41,10 @@ struct LevelArgs {
   int alternate;        // 1: odd chunks stream bottom-up (shared warm-up rows hit L2)
   int staged;           // 1: interleaved input rows staged in shared memory by TMA
   int pdl;              // host only: launch with programmatic dependent launch
+  // outputs stored only inside [keep_x0, keep_x1) x [keep_y0, keep_y1)
+  // (component grid; keep_x1 == 0: the whole level): a symmetric level's
+  // interior, its border bands come from the crop kernel
+  int keep_x0, keep_x1, keep_y0, keep_y1;
   float neg_zero;       // -0.0f (set by the host: an operand ptxas cannot fold, level_engine.cuh)
   // Row strips (multi-GPU): when halo != 0, component rows above the strip
   // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from
@@ -68,6 +72,15 @@ struct PairArgs {
 using PairLaunch = cudaError_t (*)(const PairArgs&, cudaStream_t);
 
 
+// compiled border crops of a plan (crop_engine.cuh): all sub-steps of the
+// border bands (CropTileArgs, below) with the tap tables compiled in; aw x ah
+// bounds the tile areas of the launch (shared-memory size)
+struct CropTileArgs;
+constexpr int kCropThreads = 256;  // one tile-area cell and one ghost cell per thread
+// ghost ring cells of an aw x ah tile area with ring width r
+constexpr int crop_ring_cells(int aw, int ah, int r) { return 2 * r * (aw + 2 * r) + 2 * r * ah; }
+using CropLaunch = cudaError_t (*)(const CropTileArgs&, int aw, int ah, bool pdl, cudaStream_t);
+
 // resident CTAs per SM of a launcher's vector-path kernel (0 if unknown)
 using LevelOccupancy = int (*)();
 
@@ -84,6 +97,8 @@ struct PlanEntry {
   LevelOccupancy occupancy;    // resident CTAs per SM (vector path)
   PairLaunch pair;             // levels 1+2 in one pass (forward plans with reach <= 2, CW 4)
   LevelOccupancy pair_occupancy;
+  CropLaunch crop;             // symmetric border bands, compiled taps
+  int crop_reach;              // largest reach of one sub-step (the crop kernel's ghost ring)
   // loads every kernel of the entry into the context now (lazy module
   // loading would otherwise load at first launch, which waits for running
   // kernels: a deadlock when one of them spins on work not yet launched)
@@ -129,7 +144,9 @@ struct CropTileArgs {
   CropRegion reg[4];
   const RowDesc* rows;     // nsteps * 4 (device)
   const TapDesc* taps;     // (device)
+  int w2, h2;              // the level grid (true image edges; compiled crop kernel)
 };
+
 cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, bool pdl, cudaStream_t st);
 
 // up to kMaxGenericRegions independent passes (same sub-step, different

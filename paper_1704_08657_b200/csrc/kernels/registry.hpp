@@ -11,6 +11,7 @@
 
 #include "level_engine.cuh"
 #include "pair_engine.cuh"
+#include "crop_engine.cuh"
 #include "level_types.hpp"
 
 namespace dwt2d_b200 {
@@ -110,6 +111,29 @@ int pair_occupancy() {
   return blocks;
 }
 
+template <class P>
+cudaError_t launch_crop(const CropTileArgs& a, int aw, int ah, bool pdl, cudaStream_t st) {
+  int tiles = 0;
+  for (int i = 0; i < a.nreg; ++i) tiles += a.reg[i].tiles;
+  if (tiles == 0) return cudaSuccess;
+  const int bytes = crop_smem_floats<P>(aw, ah) * 4;
+  if (bytes > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(crop_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(tiles));
+  cfg.blockDim = dim3(kCropThreads);
+  cfg.dynamicSmemBytes = size_t(bytes);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, crop_kernel<P>, a);
+}
+
 template <class P, bool kForward>
 cudaError_t preload_entry() {
   cudaFuncAttributes fa;
@@ -119,6 +143,7 @@ cudaError_t preload_entry() {
   };
   load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, false, true>));
   load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, false, false>));
+  load(reinterpret_cast<const void*>(crop_kernel<P>));
   if constexpr (kForward) {
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, true>));
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, false>));
@@ -145,6 +170,8 @@ PlanEntry make_entry() {
   e.up = M::U, e.down = M::L, e.left = M::HL, e.right = M::HR;
   e.taps_per_quad = P::kTaps;
   e.planar = &launch_level<P, false, false>;
+  e.crop = &launch_crop<P>;
+  e.crop_reach = CropGeom<P>::R;
   e.preload = &preload_entry<P, kForward>;
   if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;

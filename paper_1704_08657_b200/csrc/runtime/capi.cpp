@@ -35,8 +35,9 @@ struct Tuning {
   int tma = 1;              // DWT2D_TMA: 0 off, 1 levels >= 512 MiB, 2 every stageable level
   int pair = 1;             // DWT2D_PAIR: 0 off, 1 where level 1 is staged, 2 forced
   int pair_chunk_rows = 0;  // DWT2D_PAIR_CHUNK_ROWS (0: policy)
-  int crop_tiles = 1;       // DWT2D_CROP_TILES: symmetric border crops in one tile launch
-  int crop_core = 8;        // DWT2D_CROP_CORE: positions per crop tile
+  int crop_tiles = 2;       // DWT2D_CROP_TILES: symmetric border crops: 2 compiled crop kernel concurrent
+                            // with the fused kernel, 1 one generic tile launch after it, 0 per sub-step
+  int crop_core = 12;       // DWT2D_CROP_CORE: positions per crop tile (capped by the crop kernel's 256 cells)
   int host_band_rows = 0;   // DWT2D_HOST_BAND_ROWS: image rows per host pipeline band (0: policy)
 };
 
@@ -212,6 +213,8 @@ void prepare(const dwt2d_plan& p, gpu::LevelArgs& a, Layout layout, int chunk_ov
   a.alternate = p.tune.alternate == 0 ? 0 : p.tune.alternate == 2 ? 2 : 1;  // 2: also single-wave levels (tests)
   a.pdl = p.tune.pdl ? 1 : 0;
   a.neg_zero = -0.0f;
+  if (a.keep_x1 <= 0) a.keep_x0 = 0, a.keep_x1 = a.w2;
+  if (a.keep_y1 <= 0) a.keep_y0 = 0, a.keep_y1 = a.h2;
   const gpu::PlanEntry& e = *p.entry;
   const int cw = e.cw;
   a.nstrips = (a.w2 + gpu::kOutLanes * cw - 1) / (gpu::kOutLanes * cw);
@@ -438,9 +441,88 @@ void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStre
 // reaches at most up + down rows, resp. left + right columns, into the crop;
 // the margin keeps the crop's artificial inner edge out of every kept
 // cone). Levels too small for the crops run wholly on the generic executor.
+// Core positions per crop-kernel tile: the tile area (core + margins along
+// the band, `across` cells across it) and its ghost ring hold at most
+// kCropThreads cells, one per thread. 0: the band is too wide for the kernel.
+int crop_core_for(const dwt2d_plan& p, int margins, int across, int along_max) {
+  const int r = p.entry->crop_reach;
+  int core = std::min(p.tune.crop_core, gpu::kCropThreads / std::max(1, across) - margins);
+  core = std::min(core, along_max);
+  while (core >= 1) {
+    const int along = std::min(along_max, core + margins);
+    if (along * across <= gpu::kCropThreads && gpu::crop_ring_cells(along, across, r) <= gpu::kCropThreads) break;
+    --core;
+  }
+  return std::max(core, 0);
+}
+
+// The compiled form (crop_engine.cuh): the fused kernel stores the interior
+// only (keep window: rows [up, h2 - down), columns widened to whole lanes),
+// the crop kernel the four border bands around it, on a side stream at the
+// same time (disjoint outputs, both read only the level input).
+void run_symmetric_compiled(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+  const int w2 = a.w2, h2 = a.h2, cw = p.entry->cw;
+  const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
+  const int kl = (p.left + cw - 1) / cw * cw, kr = (p.right + cw - 1) / cw * cw;  // lane-aligned side bands
+  gpu::CropTileArgs t{};
+  for (int j = 0; j < 4; ++j) {
+    t.in[j] = a.in[j], t.in_pitch[j] = a.in_pitch[j];
+    t.out[j] = a.out[j], t.out_pitch[j] = a.out_pitch[j];
+  }
+  t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
+  t.w2 = w2, t.h2 = h2;
+  t.mlo = t.mhi = std::max(p.left + p.right, p.up + p.down);
+  t.core = crop_core_for(p, t.mlo + t.mhi, std::max(my, mx), std::max(w2, h2));
+  const int tx = (w2 + t.core - 1) / t.core, ty = (h2 + t.core - 1) / t.core;
+  t.nreg = 4;
+  t.reg[0] = gpu::CropRegion{0, 0, w2, my, 0, w2, 0, p.up, 1, tx};
+  t.reg[1] = gpu::CropRegion{0, h2 - my, w2, my, 0, w2, my - p.down, my, 1, tx};
+  t.reg[2] = gpu::CropRegion{0, 0, mx, h2, 0, kl, p.up, h2 - p.down, 0, ty};
+  t.reg[3] = gpu::CropRegion{w2 - mx, 0, mx, h2, mx - kr, mx, p.up, h2 - p.down, 0, ty};
+  const int along = std::min(std::max(w2, h2), t.core + t.mlo + t.mhi), across = std::max(my, mx);
+  SideStream& side = side_stream();
+  cuda_check(cudaEventRecord(side.fork, st), "fork");
+  cuda_check(cudaStreamWaitEvent(side.s, side.fork, 0), "fork");
+  cuda_check(p.entry->crop(t, along, across, false, side.s), "crop kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  gpu::LevelArgs in = a;
+  in.keep_x0 = kl, in.keep_x1 = w2 - kr, in.keep_y0 = p.up, in.keep_y1 = h2 - p.down;
+  launch_fused(p, in, layout, st);
+  cuda_check(cudaEventRecord(side.join, side.s), "join");
+  cuda_check(cudaStreamWaitEvent(st, side.join, 0), "join");
+}
+
+// A level too small for four border bands: the crop kernel takes all of it
+// (one region, every side a true image edge), tiled along its longer side.
+void run_symmetric_small(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
+  gpu::CropTileArgs t{};
+  for (int j = 0; j < 4; ++j) {
+    t.in[j] = a.in[j], t.in_pitch[j] = a.in_pitch[j];
+    t.out[j] = a.out[j], t.out_pitch[j] = a.out_pitch[j];
+  }
+  t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
+  t.w2 = a.w2, t.h2 = a.h2;
+  t.mlo = t.mhi = std::max(p.left + p.right, p.up + p.down);
+  const bool along_x = a.w2 >= a.h2;
+  const int n = along_x ? a.w2 : a.h2;
+  t.core = crop_core_for(p, t.mlo + t.mhi, along_x ? a.h2 : a.w2, n);
+  t.nreg = 1;
+  t.reg[0] = gpu::CropRegion{0, 0, a.w2, a.h2, 0, a.w2, 0, a.h2, along_x ? 1 : 0, (n + t.core - 1) / t.core};
+  const int along = std::min(n, t.core + t.mlo + t.mhi), across = along_x ? a.h2 : a.w2;
+  cuda_check(p.entry->crop(t, along_x ? along : across, along_x ? across : along, p.tune.pdl != 0, st),
+             "crop kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
   const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
-  if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
+  const bool compiled = p.tune.crop_tiles == 2 && p.entry->crop;
+  if (a.h2 < 2 * my || a.w2 < 2 * mx) {
+    if (compiled && crop_core_for(p, 2 * std::max(p.left + p.right, p.up + p.down), std::min(a.w2, a.h2),
+                                  std::max(a.w2, a.h2)) > 0)
+      return run_symmetric_small(p, a, layout, st);
+    return run_generic(p, a, layout, st);
+  }
   const int w2 = a.w2, h2 = a.h2;
   if (!p.tune.crop_tiles) {  // one generic launch per sub-step over the four crops
     // the crops' intermediate sub-steps run on a side stream while the fused
@@ -455,6 +537,9 @@ void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, 
                         st, &fused);
     return;
   }
+  if (compiled && crop_core_for(p, 2 * std::max(p.left + p.right, p.up + p.down), std::max(my, mx),
+                                std::max(a.w2, a.h2)) > 0)
+    return run_symmetric_compiled(p, a, layout, st);
   // all sub-steps of the four crops in one launch (crop_tile_kernel): tiles of
   // 8 positions along each crop's long side plus margins of the program's
   // cumulative reach, whose values only the discarded margins depend on

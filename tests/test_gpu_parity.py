@@ -393,20 +393,25 @@ def test_symmetric_reconstruction(dwt, cuda, w):
                                      ("cdf53", "nonseparable-polyconvolution", True),
                                      ("dd137", "nonseparable-lifting", False), ("cdf97", "inverse-lifting", False),
                                      ("dd137", "separable-lifting", True)])
-@pytest.mark.parametrize("tiles", ["1", "0"])
+@pytest.mark.parametrize("tiles", ["2", "1", "0"])
 def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, tiles, monkeypatch):
-    """Symmetric extension on the fused kernel + generic border crops equals
-    the all-generic per-step symmetric executor bit for bit: planar run(),
+    """Symmetric extension on the fused kernel + border crops equals the
+    all-generic per-step symmetric executor bit for bit: planar run(),
     forward level from the image, inverse level to the image, incl. odd
-    (scalar-path) widths and grids just above the crop threshold."""
+    (scalar-path) widths, grids just above the crop threshold and levels too
+    small for border bands (1 x 1 up to 23 x 300 components)."""
     import torch
-    # one tile launch, or one launch per sub-step
+    # compiled crop kernel beside the fused kernel's interior, one generic
+    # tile launch, or one generic launch per sub-step
     fused = dwt.Plan(w, s, optimized=opt, extension="symmetric").tune(crop_tiles=int(tiles))
     monkeypatch.setenv("DWT2D_FORCE_GENERIC", "1")
     gen = dwt.Plan(w, s, optimized=opt, extension="symmetric")
     monkeypatch.delenv("DWT2D_FORCE_GENERIC")
     assert fused.info["generic"] == 0 and gen.info["generic"] == 1
-    for (w2, h2) in [(64, 48), (150, 101), (300, 40), (40, 300), (33, 33)]:
+    sizes = [(64, 48), (150, 101), (300, 40), (40, 300), (33, 33)]
+    if tiles == "2":
+        sizes += [(1, 1), (2, 3), (5, 4), (17, 9), (23, 300), (300, 7), (24, 24), (96, 13)]
+    for (w2, h2) in sizes:
         planes = _to_dev(O.split(O.random_image(2 * w2, 2 * h2, 7 + w2)), cuda)
         a, b = fused.run(planes), gen.run(planes)
         for j in range(4):
