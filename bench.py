@@ -104,6 +104,21 @@ def ncu_traffic(name="ncu_level1_summary.json"):
     return None
 
 
+def roofline_entry(achieved, peak, peak_src, dom_bytes, dom_ms, kernel_desc, traffic):
+    """The dominant kernel against the measured copy bandwidth: `achieved` /
+    `frac` on the reference's algorithmic bytes (8 B/pixel/level), and — with
+    the committed ncu capture's DRAM bytes per launch — the same launch on the
+    bytes it really moves (the fused level pair never writes or re-reads LL_1,
+    so its DRAM traffic is ~0.79x the algorithmic bytes and the algorithmic
+    rate can exceed the copy rate)."""
+    e = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+         "traffic": traffic, "algorithmic_bytes": dom_bytes, "kernel": kernel_desc, "peak_source": peak_src}
+    if traffic:
+        e["achieved_dram"] = traffic / (dom_ms * 1e-3) / 1e9
+        e["frac_dram"] = e["achieved_dram"] / peak
+    return e
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -468,11 +483,9 @@ def main():
             "ns_per_pixel": r["ms_per_step"] * 1e6 / pixels,
             "pyramid_hbm_gbs_per_gpu": pyr_bytes / (r["ms_per_step"] * 1e-3) / 1e9,
             "levels_ms": r["levels_ms"],
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": ncu_traffic("ncu_pair_summary.json" if r["fused12"] else "ncu_level1_summary.json")
-                         if (wl == "c3" and n == 1) else None,
-                         "algorithmic_bytes": dom_bytes, "kernel": kernel_desc, "peak_source": peak_src},
+            "roofline": roofline_entry(achieved, peak, peak_src, dom_bytes, r["dom_ms"], kernel_desc,
+                                       ncu_traffic("ncu_pair_summary.json" if r["fused12"] else "ncu_level1_summary.json")
+                                       if (wl == "c3" and n == 1) else None),
             "e2e": {"value": pixels / e2e_s / 1e9, "unit": "Gpixel/s",
                     "h2d_bytes_per_step": int(W * Hs * 4), "d2h_bytes_per_step": int(W * Hs * 4),
                     "api": ("dwt2d_forward_mallat_host (C ABI), pinned host buffers" if not sharded else

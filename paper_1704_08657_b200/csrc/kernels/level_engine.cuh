@@ -768,7 +768,7 @@ struct RowWriter {
   int xc, kx0, kx1;  // columns stored: [kx0, kx1) (the keep window, LevelArgs)
 
   __device__ __forceinline__ void init(const LevelArgs& a, int xc_, int first_row) {
-    xc = xc_, kx0 = a.keep_x0, kx1 = a.keep_x1;
+    xc = xc_, kx0 = a.keep_x0, kx1 = a.keep_x1 > 0 ? a.keep_x1 : a.w2;
     sfor<0, 4>([&](auto J_) {
       constexpr int j = decltype(J_)::value;
       if constexpr (IL) {
@@ -896,7 +896,7 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   const int rows = (y1 - y0) + M::U + M::L;
   const int iters = (rows + UNR - 1) / UNR * UNR;
   bool out_lane = lane >= 1 && lane <= kOutLanes;
-  const int ys0 = max(y0, a.keep_y0), ys1 = min(y1, a.keep_y1);  // rows stored
+  const int ys0 = max(y0, a.keep_y0), ys1 = min(y1, a.keep_y1 > 0 ? a.keep_y1 : a.h2);  // rows stored
 
   float ring[S + 1][D][4][CW];
   sfor<1, S + 1>([&](auto B_) {

@@ -9,7 +9,10 @@
 namespace dwt2d_b200 {
 namespace gpu {
 
-constexpr int kWarpsPerCta = 4;
+#ifndef DWT2D_WARPS_PER_CTA
+#define DWT2D_WARPS_PER_CTA 4
+#endif
+constexpr int kWarpsPerCta = DWT2D_WARPS_PER_CTA;
 constexpr int kOutLanes = 30;  // lanes 1..30 store, 0 and 31 are halo
 
 struct TapDesc {
@@ -42,7 +45,7 @@ struct LevelArgs {
   int staged;           // 1: interleaved input rows staged in shared memory by TMA
   int pdl;              // host only: launch with programmatic dependent launch
   // outputs stored only inside [keep_x0, keep_x1) x [keep_y0, keep_y1)
-  // (component grid; keep_x1 == 0: the whole level): a symmetric level's
+  // (component grid; keep_x1 / keep_y1 == 0: to the level's edge): a symmetric level's
   // interior, its border bands come from the crop kernel
   int keep_x0, keep_x1, keep_y0, keep_y1;
   float neg_zero;       // -0.0f (set by the host: an operand ptxas cannot fold, level_engine.cuh)

@@ -57,7 +57,7 @@ int main(int argc, char** argv) {
     a.nstrips = (a.w2 + kOutLanes * 4 - 1) / (kOutLanes * 4);
     a.chunk_rows = 64;
     a.nchunks = (a.h2 + 63) / 64;
-    level_kernel<P, 2, true, false, true><<<(a.nstrips * a.nchunks + 3) / 4, 128>>>(a);
+    level_kernel<P, 2, true, false, true><<<(a.nstrips * a.nchunks + kWarpsPerCta - 1) / kWarpsPerCta, kWarpsPerCta * 32>>>(a);
   }
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(ref.data(), mal, n * 4, cudaMemcpyDeviceToHost));
@@ -69,11 +69,12 @@ int main(int argc, char** argv) {
     const int smem = staged_bytes<4>();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarpsPerCta * 32, smem));
     PairArgs t{};
     t.l1 = level_args(img, W, W / 2, H / 2, nullptr, 0);
     t.l2 = level_args(nullptr, 0, W / 4, H / 4, ll2, W / 4);
     t.l1.staged = 1;
+    t.l1.neg_zero = -0.0f;
     t.nstrips = (t.l1.w2 + kPairLanes * 4 - 1) / (kPairLanes * 4);
     const long long resident = (long long)occ * kWarpsPerCta * sms;
     const long long per_wave = std::max<long long>(1, resident / t.nstrips);
@@ -83,22 +84,22 @@ int main(int argc, char** argv) {
     if (chunk_override) chunk = chunk_override;
     t.chunk_rows = int(std::min<long long>(chunk, span));
     t.nchunks = (span + t.chunk_rows - 1) / t.chunk_rows;
-    const unsigned blocks = unsigned((t.nstrips * t.nchunks + 3) / 4);
+    const unsigned blocks = unsigned((t.nstrips * t.nchunks + kWarpsPerCta - 1) / kWarpsPerCta);
     CK(cudaMemset(mal, 0, n * 4));
     CK(cudaMemset(ll2, 0, n / 4));
-    kern<<<blocks, 128, smem>>>(t);
+    kern<<<blocks, kWarpsPerCta * 32, smem>>>(t);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(got.data(), mal, n * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(got_ll.data(), ll2, n / 4, cudaMemcpyDeviceToHost));
     long long bad = 0;
     for (size_t i = 0; i < n; ++i) bad += memcmp(&got[i], &ref[i], 4) != 0;
     for (size_t i = 0; i < n / 16; ++i) bad += memcmp(&got_ll[i], &ref_ll[i], 4) != 0;
-    for (int i = 0; i < 3; ++i) kern<<<blocks, 128, smem>>>(t);
+    for (int i = 0; i < 3; ++i) kern<<<blocks, kWarpsPerCta * 32, smem>>>(t);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0), cudaEventCreate(&e1);
     const int iters = 20;
     cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) kern<<<blocks, 128, smem>>>(t);
+    for (int i = 0; i < iters; ++i) kern<<<blocks, kWarpsPerCta * 32, smem>>>(t);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms = 0;
@@ -106,14 +107,13 @@ int main(int argc, char** argv) {
     ms /= iters;
     // algorithmic bytes: 8 B per pixel per level (reference bench.cpp:84-85)
     const double alg = 8.0 * n * 1.25;
-    printf("%-14s regs %3d occ %d chunk %4d  %8.2f us  %7.1f GB/s alg  mismatches %lld\n", name, fa.numRegs, occ,
+    printf("wpc %d %-14s regs %3d occ %2d chunk %4d  %8.2f us  %7.1f GB/s alg  mismatches %lld\n", kWarpsPerCta, name, fa.numRegs, occ,
            t.chunk_rows, ms * 1e3, alg / (ms * 1e-3) / 1e9, bad);
   };
   for (int rep = 0; rep < 2; ++rep) {
     run("VF0 scalar", k_pair<0, 1>, 0);
     run("VF1 (c,c+1)", k_pair<1, 1>, 0);
     run("VF2 (c,c+2)", k_pair<2, 1>, 0);
-    run("VF2 minb3", k_pair<2, 3>, 0);
   }
   return 0;
 }
