@@ -289,6 +289,20 @@ DWT2D_B200_API int dwt2d_forward_mallat_ex(const dwt2d_plan* plan, const float* 
                                            int width, int height, int levels, float* out,
                                            size_t out_pitch, void* scratch, void* const* events,
                                            void* stream);
+/* A batch of independent images (images need no exchange, they
+ * run as replicas): n forward pyramids of one geometry, device buffers.
+ * Image i (images[i] -> outs[i]) runs on devices[i % ndev] and is ordered
+ * after / before the work on streams[i % ndev] (NULL array or entry: that
+ * device's legacy default stream); devices == NULL: the current device. On
+ * each device the batch's images overlap on up to four library streams
+ * forked from and joined back to that stream (event fork/join, capturable
+ * into a CUDA graph); workspaces come from the stream-ordered allocator. No
+ * reference counterpart: a batch driver over the reference's per-image
+ * compile/run calls (executor.hpp:196-238). */
+DWT2D_B200_API int dwt2d_forward_mallat_batch(const dwt2d_plan* plan, int n, const float* const* images,
+                                              size_t pitch, int width, int height, int levels,
+                                              float* const* outs, size_t out_pitch, int ndev,
+                                              const int* devices, void* const* streams);
 DWT2D_B200_API int dwt2d_event_create(void** event);
 DWT2D_B200_API int dwt2d_event_destroy(void* event);
 DWT2D_B200_API int dwt2d_event_elapsed_ms(void* start, void* end, float* ms);

@@ -1719,6 +1719,74 @@ int dwt2d_forward_mallat_ex(const dwt2d_plan* p, const float* image, size_t pitc
   });
 }
 
+namespace {
+// Library streams of a batch on one device (per thread, per device): images
+// of the batch overlap on them, forked from and joined back to the caller's
+// stream with events.
+struct BatchLanes {
+  static constexpr int kLanes = 4;
+  cudaStream_t s[kLanes] = {};
+  cudaEvent_t fork = nullptr, join[kLanes] = {};
+};
+BatchLanes& batch_lanes() {
+  static thread_local std::unique_ptr<BatchLanes> per_dev[kMaxDevices];
+  std::unique_ptr<BatchLanes>& b = per_dev[current_device()];
+  if (!b) {
+    auto n = std::make_unique<BatchLanes>();
+    cuda_check(cudaEventCreateWithFlags(&n->fork, cudaEventDisableTiming), "batch fork event");
+    for (int i = 0; i < BatchLanes::kLanes; ++i) {
+      cuda_check(cudaStreamCreateWithFlags(&n->s[i], cudaStreamNonBlocking), "batch stream");
+      cuda_check(cudaEventCreateWithFlags(&n->join[i], cudaEventDisableTiming), "batch join event");
+    }
+    b = std::move(n);
+  }
+  return *b;
+}
+}  // namespace
+
+int dwt2d_forward_mallat_batch(const dwt2d_plan* p, int n, const float* const* images, size_t pitch, int W, int H,
+                               int levels, float* const* outs, size_t out_pitch, int ndev, const int* devices,
+                               void* const* streams) {
+  return guard([&] {
+    require_plan(p);
+    if (n < 0 || (n > 0 && (!images || !outs))) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
+    check_pyramid(W, H, levels);
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    if (devices && ndev < 1) fail(DWT2D_EINVAL, "batch: ndev must be at least 1");
+    if (!devices) ndev = 1;
+    for (int i = 0; i < n; ++i)
+      if (!images[i] || !outs[i]) fail(DWT2D_EINVAL, "batch: null image or output");
+    for (int d = 0; d < ndev && d < n; ++d) {
+      int dev = 0;
+      if (devices) dev = devices[d];
+      else cuda_check(cudaGetDevice(&dev), "current device");
+      DeviceGuard g(dev);
+      const cudaStream_t st = streams ? as_stream(streams[d]) : cudaStream_t(nullptr);
+      std::vector<int> mine;
+      for (int i = d; i < n; i += ndev) mine.push_back(i);
+      auto run = [&](int i, cudaStream_t s) {
+        Workspace ws;
+        get_workspace(ws, nullptr, W, H, levels, s);
+        forward_mallat(*p, images[i], pitch, W, H, levels, outs[i], out_pitch, ws.ptr, s);
+      };
+      if (mine.size() == 1) {
+        run(mine[0], st);
+        continue;
+      }
+      BatchLanes& b = batch_lanes();
+      const int lanes = std::min<int>(BatchLanes::kLanes, int(mine.size()));
+      cuda_check(cudaEventRecord(b.fork, st), "batch fork");
+      for (int k = 0; k < lanes; ++k) cuda_check(cudaStreamWaitEvent(b.s[k], b.fork, 0), "batch fork");
+      for (size_t k = 0; k < mine.size(); ++k) run(mine[k], b.s[k % lanes]);
+      for (int k = 0; k < lanes; ++k) {
+        cuda_check(cudaEventRecord(b.join[k], b.s[k]), "batch join");
+        cuda_check(cudaStreamWaitEvent(st, b.join[k], 0), "batch join");
+      }
+    }
+  });
+}
+
 int dwt2d_event_create(void** ev) {
   return guard([&] {
     if (!ev) fail(DWT2D_EINVAL, "null argument");

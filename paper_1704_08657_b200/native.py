@@ -120,6 +120,8 @@ _SIGS = {
     "dwt2d_workspace_bytes": (_sz, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),
+    "dwt2d_forward_mallat_batch": (ctypes.c_int, [_p, ctypes.c_int, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                  _p, _sz, ctypes.c_int, _p, _p]),
     "dwt2d_forward_mallat_ex": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                                _p, ctypes.POINTER(ctypes.c_void_p), _p]),
     "dwt2d_event_create": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p)]),

@@ -297,6 +297,42 @@ class Plan:
                                                   _stream_handle(stream)))
         return out
 
+    def forward_mallat_batch(self, images, levels: int, outs=None, devices=None, streams=None):
+        """Forward pyramids of a batch of equally sized CUDA images
+        (dwt2d_forward_mallat_batch): image i runs on devices[i % len(devices)]
+        (its tensor must live there), overlapping with the batch's other images
+        on library streams; ordered on streams[i % len(devices)] (torch
+        streams or raw handles; default: each device's current torch stream)."""
+        import torch
+        if not images:
+            return []
+        H, W = images[0].shape
+        pitch = _dev(images[0], "image")[1]
+        if outs is None:
+            outs = [torch.empty((H, W), dtype=torch.float32, device=im.device) for im in images]
+        opitch = _dev(outs[0], "out")[1]
+        for im, o in zip(images, outs):
+            if tuple(im.shape) != (H, W) or tuple(o.shape) != (H, W):
+                raise ValueError("batch: images and outputs must share one shape")
+            if _dev(im, "image")[1] != pitch or _dev(o, "out")[1] != opitch:
+                raise ValueError("batch: images (and outputs) must share one row pitch")
+        devs = [images[0].device.index or 0] if devices is None else [int(d) for d in devices]
+        for i, (im, o) in enumerate(zip(images, outs)):
+            want = devs[i % len(devs)]
+            if im.device.index != want or o.device.index != want:
+                raise ValueError(f"batch: image {i} and its output must be on cuda:{want}")
+        if streams is None:
+            streams = [torch.cuda.current_stream(torch.device("cuda", d)) for d in devs]
+        if len(streams) != len(devs):
+            raise ValueError("batch: one stream per device")
+        n = len(images)
+        ims = (ctypes.c_void_p * n)(*[im.data_ptr() for im in images])
+        ous = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+        dv = (ctypes.c_int * len(devs))(*devs)
+        sts = (ctypes.c_void_p * len(devs))(*[_stream_handle(s) for s in streams])
+        N.check(N.lib.dwt2d_forward_mallat_batch(self._h, n, ims, pitch, W, H, levels, ous, opitch, len(devs), dv, sts))
+        return outs
+
     def inverse_mallat(self, coeffs, levels: int, image=None, scratch=None, stream=None):
         import torch
         H, W = coeffs.shape
