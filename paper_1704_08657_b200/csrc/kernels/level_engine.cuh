@@ -988,12 +988,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, MIN_CTAS)
 level_kernel(const LevelArgs a) {
   // PDL (registry.hpp: launch_level): the previous kernel's results are
   // visible after the wait; the next launch may begin once every CTA of this
-  // grid has started. Both are no-ops for a normal launch.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // grid has started. Both are no-ops for a normal launch. wait_end: the
+  // previous kernel (a symmetric level's crop kernel, which itself waited for
+  // the level's input) computes something this launch does not read, so the
+  // wait moves to the end: the two run together, and this grid still
+  // completes only after its predecessor (the next level waits on it).
+  if (!a.wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
-  if (wid >= a.nstrips * a.nchunks) return;  // warp-uniform
-  level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && IN_IL && P::kAlt, STAGED>(a, wid);
+  if (wid < a.nstrips * a.nchunks)  // warp-uniform
+    level_dispatch<P, PF, IN_IL, OUT_IL, VEC, false, VEC && IN_IL && P::kAlt, STAGED>(a, wid);
+  if (a.wait_end) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace gpu

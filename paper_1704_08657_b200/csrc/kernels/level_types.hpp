@@ -48,6 +48,7 @@ struct LevelArgs {
   // (component grid; keep_x1 / keep_y1 == 0: to the level's edge): a symmetric level's
   // interior, its border bands come from the crop kernel
   int keep_x0, keep_x1, keep_y0, keep_y1;
+  int wait_end;         // PDL wait at the end of the kernel instead of its start (level_engine.cuh)
   float neg_zero;       // -0.0f (set by the host: an operand ptxas cannot fold, level_engine.cuh)
   // Row strips (multi-GPU): when halo != 0, component rows above the strip
   // (y < 0) come from halo_top (row y + up) and rows below (y >= h2) from

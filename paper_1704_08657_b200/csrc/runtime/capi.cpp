@@ -460,10 +460,30 @@ int crop_core_for(const dwt2d_plan& p, int margins, int across, int along_max) {
 // only (keep window: rows [up, h2 - down), columns widened to whole lanes),
 // the crop kernel the four border bands around it, on a side stream at the
 // same time (disjoint outputs, both read only the level input).
+// Crop geometry of the compiled kernel. Its ghost cells are filled only at
+// true image edges, so garbage enters a tile only through its other edges
+// and spreads at most the level's cumulative reach: a kept row r < up of the
+// top band reads rows <= r + down, so up + down + 2 rows suffice (the
+// generic crops, which reflect at the crop's inner edge too, take twice the
+// reach + 4), the side bands their lane-aligned kept columns plus the reach
+// + 2, and tiles along a band a margin of the reach + 1.
+struct CropGeometry {
+  int my, mx, kl, kr, margin;
+};
+CropGeometry crop_geometry(const dwt2d_plan& p) {
+  const int cw = p.entry->cw;
+  CropGeometry g;
+  g.kl = (p.left + cw - 1) / cw * cw, g.kr = (p.right + cw - 1) / cw * cw;  // lane-aligned side bands
+  g.my = p.up + p.down + 2;
+  g.mx = std::max(g.kl, g.kr) + std::max(p.left, p.right) + 2;
+  g.margin = std::max(std::max(p.left, p.right), std::max(p.up, p.down)) + 1;
+  return g;
+}
+
 void run_symmetric_compiled(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
-  const int w2 = a.w2, h2 = a.h2, cw = p.entry->cw;
-  const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
-  const int kl = (p.left + cw - 1) / cw * cw, kr = (p.right + cw - 1) / cw * cw;  // lane-aligned side bands
+  const int w2 = a.w2, h2 = a.h2;
+  const CropGeometry cg = crop_geometry(p);
+  const int my = cg.my, mx = cg.mx, kl = cg.kl, kr = cg.kr;
   gpu::CropTileArgs t{};
   for (int j = 0; j < 4; ++j) {
     t.in[j] = a.in[j], t.in_pitch[j] = a.in_pitch[j];
@@ -471,7 +491,7 @@ void run_symmetric_compiled(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout
   }
   t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
   t.w2 = w2, t.h2 = h2;
-  t.mlo = t.mhi = std::max(p.left + p.right, p.up + p.down);
+  t.mlo = t.mhi = cg.margin;
   t.core = crop_core_for(p, t.mlo + t.mhi, std::max(my, mx), std::max(w2, h2));
   const int tx = (w2 + t.core - 1) / t.core, ty = (h2 + t.core - 1) / t.core;
   t.nreg = 4;
@@ -480,16 +500,28 @@ void run_symmetric_compiled(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout
   t.reg[2] = gpu::CropRegion{0, 0, mx, h2, 0, kl, p.up, h2 - p.down, 0, ty};
   t.reg[3] = gpu::CropRegion{w2 - mx, 0, mx, h2, mx - kr, mx, p.up, h2 - p.down, 0, ty};
   const int along = std::min(std::max(w2, h2), t.core + t.mlo + t.mhi), across = std::max(my, mx);
-  SideStream& side = side_stream();
-  cuda_check(cudaEventRecord(side.fork, st), "fork");
-  cuda_check(cudaStreamWaitEvent(side.s, side.fork, 0), "fork");
-  cuda_check(p.entry->crop(t, along, across, false, side.s), "crop kernel launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
   gpu::LevelArgs in = a;
   in.keep_x0 = kl, in.keep_x1 = w2 - kr, in.keep_y0 = p.up, in.keep_y1 = h2 - p.down;
+  // Large levels: the crops on a side stream, fully concurrent with the fused
+  // kernel's waves. Smaller levels, where a fork/join costs as much as the
+  // level: one stream, crop kernel first, the fused kernel launched behind it
+  // by PDL with its wait at the end (wait_end), so the two overlap and the
+  // PDL chain to the next level stays intact.
+  if (!p.tune.pdl || size_t(w2) * size_t(h2) * 16 >= (size_t(256) << 20)) {
+    SideStream& side = side_stream();
+    cuda_check(cudaEventRecord(side.fork, st), "fork");
+    cuda_check(cudaStreamWaitEvent(side.s, side.fork, 0), "fork");
+    cuda_check(p.entry->crop(t, along, across, false, side.s), "crop kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    launch_fused(p, in, layout, st);
+    cuda_check(cudaEventRecord(side.join, side.s), "join");
+    cuda_check(cudaStreamWaitEvent(st, side.join, 0), "join");
+    return;
+  }
+  cuda_check(p.entry->crop(t, along, across, true, st), "crop kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  in.wait_end = 1;
   launch_fused(p, in, layout, st);
-  cuda_check(cudaEventRecord(side.join, side.s), "join");
-  cuda_check(cudaStreamWaitEvent(st, side.join, 0), "join");
 }
 
 // A level too small for four border bands: the crop kernel takes all of it
@@ -502,7 +534,7 @@ void run_symmetric_small(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
   }
   t.in_il = layout == kFromImage, t.out_il = layout == kToImage;
   t.w2 = a.w2, t.h2 = a.h2;
-  t.mlo = t.mhi = std::max(p.left + p.right, p.up + p.down);
+  t.mlo = t.mhi = crop_geometry(p).margin;
   const bool along_x = a.w2 >= a.h2;
   const int n = along_x ? a.w2 : a.h2;
   t.core = crop_core_for(p, t.mlo + t.mhi, along_x ? a.h2 : a.w2, n);
@@ -517,12 +549,17 @@ void run_symmetric_small(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout la
 void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cudaStream_t st) {
   const int my = 2 * (p.up + p.down) + 4, mx = 2 * (p.left + p.right) + 4;
   const bool compiled = p.tune.crop_tiles == 2 && p.entry->crop;
-  if (a.h2 < 2 * my || a.w2 < 2 * mx) {
-    if (compiled && crop_core_for(p, 2 * std::max(p.left + p.right, p.up + p.down), std::min(a.w2, a.h2),
-                                  std::max(a.w2, a.h2)) > 0)
-      return run_symmetric_small(p, a, layout, st);
-    return run_generic(p, a, layout, st);
+  if (compiled) {
+    const CropGeometry cg = crop_geometry(p);
+    if (a.h2 < 2 * cg.my || a.w2 < 2 * cg.mx) {
+      if (crop_core_for(p, 2 * cg.margin, std::min(a.w2, a.h2), std::max(a.w2, a.h2)) > 0)
+        return run_symmetric_small(p, a, layout, st);
+      return run_generic(p, a, layout, st);
+    }
+    if (crop_core_for(p, 2 * cg.margin, std::max(cg.my, cg.mx), std::max(a.w2, a.h2)) > 0)
+      return run_symmetric_compiled(p, a, layout, st);
   }
+  if (a.h2 < 2 * my || a.w2 < 2 * mx) return run_generic(p, a, layout, st);
   const int w2 = a.w2, h2 = a.h2;
   if (!p.tune.crop_tiles) {  // one generic launch per sub-step over the four crops
     // the crops' intermediate sub-steps run on a side stream while the fused
@@ -537,9 +574,6 @@ void run_symmetric(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, 
                         st, &fused);
     return;
   }
-  if (compiled && crop_core_for(p, 2 * std::max(p.left + p.right, p.up + p.down), std::max(my, mx),
-                                std::max(a.w2, a.h2)) > 0)
-    return run_symmetric_compiled(p, a, layout, st);
   // all sub-steps of the four crops in one launch (crop_tile_kernel): tiles of
   // 8 positions along each crop's long side plus margins of the program's
   // cumulative reach, whose values only the discarded margins depend on

@@ -410,7 +410,8 @@ def test_symmetric_fused_with_border_crops_bit_exact(dwt, cuda, w, s, opt, tiles
     assert fused.info["generic"] == 0 and gen.info["generic"] == 1
     sizes = [(64, 48), (150, 101), (300, 40), (40, 300), (33, 33)]
     if tiles == "2":
-        sizes += [(1, 1), (2, 3), (5, 4), (17, 9), (23, 300), (300, 7), (24, 24), (96, 13)]
+        sizes += [(1, 1), (2, 3), (5, 4), (17, 9), (23, 300), (300, 7), (24, 24), (96, 13), (16, 12), (17, 13),
+                  (15, 300), (300, 11)]
     for (w2, h2) in sizes:
         planes = _to_dev(O.split(O.random_image(2 * w2, 2 * h2, 7 + w2)), cuda)
         a, b = fused.run(planes), gen.run(planes)
