@@ -738,9 +738,11 @@ struct Workspace {
   float* ptr = nullptr;
   bool owned = false;
   cudaStream_t st = nullptr;
-  ~Workspace() {
+  void release() {
     if (owned && ptr) cudaFreeAsync(ptr, st);
+    ptr = nullptr, owned = false;
   }
+  ~Workspace() { release(); }
 };
 
 void get_workspace(Workspace& w, void* scratch, int W, int H, int levels, cudaStream_t st) {
@@ -1799,23 +1801,31 @@ int dwt2d_forward_mallat_batch(const dwt2d_plan* p, int n, const float* const* i
       const cudaStream_t st = streams ? as_stream(streams[d]) : cudaStream_t(nullptr);
       std::vector<int> mine;
       for (int i = d; i < n; i += ndev) mine.push_back(i);
-      auto run = [&](int i, cudaStream_t s) {
-        Workspace ws;
-        get_workspace(ws, nullptr, W, H, levels, s);
-        forward_mallat(*p, images[i], pitch, W, H, levels, outs[i], out_pitch, ws.ptr, s);
-      };
-      if (mine.size() == 1) {
-        run(mine[0], st);
-        continue;
+      // Images up to 32 MiB overlap on the library's lanes (their deep levels
+      // are latency-bound: 16 x 2048^2 0.634 vs 0.834 ms sequential); larger
+      // ones run in order on the caller's stream, where each pyramid keeps its
+      // LL bands in L2 (8 x 4096^2: 0.70 ms in order, 0.88 ms overlapped).
+      // scripts/probe_batch.py. One workspace per lane.
+      const bool overlap = mine.size() > 1 && size_t(W) * size_t(H) * 4 <= (size_t(32) << 20);
+      const int lanes = overlap ? std::min<int>(BatchLanes::kLanes, int(mine.size())) : 1;
+      BatchLanes* b = overlap ? &batch_lanes() : nullptr;
+      std::vector<Workspace> ws(lanes);
+      auto lane_stream = [&](int k) { return b ? b->s[k] : st; };
+      if (b) {
+        cuda_check(cudaEventRecord(b->fork, st), "batch fork");
+        for (int k = 0; k < lanes; ++k) cuda_check(cudaStreamWaitEvent(b->s[k], b->fork, 0), "batch fork");
       }
-      BatchLanes& b = batch_lanes();
-      const int lanes = std::min<int>(BatchLanes::kLanes, int(mine.size()));
-      cuda_check(cudaEventRecord(b.fork, st), "batch fork");
-      for (int k = 0; k < lanes; ++k) cuda_check(cudaStreamWaitEvent(b.s[k], b.fork, 0), "batch fork");
-      for (size_t k = 0; k < mine.size(); ++k) run(mine[k], b.s[k % lanes]);
+      // after the fork: inside a capture the lanes are capturing by now
+      for (int k = 0; k < lanes; ++k) get_workspace(ws[k], nullptr, W, H, levels, lane_stream(k));
+      for (size_t k = 0; k < mine.size(); ++k)
+        forward_mallat(*p, images[mine[k]], pitch, W, H, levels, outs[mine[k]], out_pitch, ws[k % lanes].ptr,
+                       lane_stream(int(k % lanes)));
       for (int k = 0; k < lanes; ++k) {
-        cuda_check(cudaEventRecord(b.join[k], b.s[k]), "batch join");
-        cuda_check(cudaStreamWaitEvent(st, b.join[k], 0), "batch join");
+        ws[k].release();  // before the join: a capture must not end with work on an unjoined lane
+        if (b) {
+          cuda_check(cudaEventRecord(b->join[k], b->s[k]), "batch join");
+          cuda_check(cudaStreamWaitEvent(st, b->join[k], 0), "batch join");
+        }
       }
     }
   });

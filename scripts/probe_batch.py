@@ -1,6 +1,8 @@
 """Image-batch throughput on one GPU: n independent pyramids through
 dwt2d_forward_mallat_batch (overlapping on library streams) vs one
-forward_mallat per image on one stream, CUDA events, median of 10:
+forward_mallat per image on one stream, each captured once into a CUDA graph
+and replayed (device time; eager calls of small images are host-bound),
+CUDA events, median of 10:
     python scripts/probe_batch.py"""
 import statistics
 import sys
@@ -25,15 +27,21 @@ for n, size, L in ((64, 512, 8), (64, 1024, 8), (16, 2048, 8), (8, 4096, 8)):
         plan.forward_mallat_batch(imgs, L, outs=outs)
 
     res = {}
+    st = torch.cuda.Stream()
     for name, fn in (("sequential", seq), ("batch", bat)):
-        fn()
-        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            fn()  # warm-up: workspaces in the stream-ordered pool
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
         ts = []
         for _ in range(10):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
+            with torch.cuda.stream(st):
+                a.record()
+                g.replay()
+                b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b))
         res[name] = statistics.median(ts)

@@ -65,7 +65,7 @@ def gbs(W, H, ms, levels=1):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r01_configs.jsonl"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r02_configs.jsonl"))
     a = ap.parse_args()
     reps = 11 if a.quick else 101
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
