@@ -856,17 +856,33 @@ struct RowWriter {
 // (row index and lane column only: no per-band pointers or pitches held in
 // registers: fewer live registers in the register-bound fused level pair;
 // in the single-level kernels it measured neutral to slower).
-template <int CW, bool UPW = false>
+// The LL band (j = 0) of the last level of a pass is the next launch's
+// input: with KEEP its stores carry an L2 evict_last policy, so it outlives
+// the evict-first detail bands streaming past it in the 126 MB L2 (the level
+// pair writes 64 MiB of LL_2 among 1 GB of detail bands at 16384^2).
+template <int CW, bool UPW = false, bool KEEP = false>
 struct LeanRowWriter {
   int xc, y;
-  __device__ __forceinline__ void init(int xc_, int first_row) { xc = xc_, y = first_row; }
+  unsigned long long keep;  // L2 cache policy (KEEP)
+  __device__ __forceinline__ void init(int xc_, int first_row) {
+    xc = xc_, y = first_row;
+    if constexpr (KEEP) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+  }
   __device__ __forceinline__ void advance() { y += UPW ? -1 : 1; }
   template <int J0>
   __device__ __forceinline__ void store_from(const LevelArgs& a, const float (&v)[4][CW]) {
     sfor<J0, 4>([&](auto J_) {
       constexpr int j = decltype(J_)::value;
       float* q = a.out[j] + (long long)y * a.out_pitch[j] + xc;
-      if constexpr (CW == 4)
+      if constexpr (KEEP && j == 0 && CW == 2)
+        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(q), "f"(v[j][0]), "f"(v[j][1]),
+                     "l"(keep)
+                     : "memory");
+      else if constexpr (KEEP && j == 0 && CW == 4)
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(q), "f"(v[j][0]),
+                     "f"(v[j][1]), "f"(v[j][2]), "f"(v[j][3]), "l"(keep)
+                     : "memory");
+      else if constexpr (CW == 4)
         st_vec(q, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
       else
         st_vec(q, make_float2(v[j][0], v[j][1]), j != 0);

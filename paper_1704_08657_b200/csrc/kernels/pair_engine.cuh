@@ -80,7 +80,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
   rd.init(a1, xc1, n01, rows1);
   LeanRowWriter<CW1> w1;
   w1.init(xc1, yfirst1);
-  LeanRowWriter<CW2> w2;
+  LeanRowWriter<CW2, false, true> w2;  // LL_2 (the next launch's input) kept in L2
   w2.init(xc2, yfirst2);
   const bool st1 = core && xc1 + CW1 <= a1.w2;
   const bool st2 = core && xc2 + CW2 <= a2.w2;

@@ -842,17 +842,21 @@ void forward_mallat(const dwt2d_plan& p, const float* image, size_t pitch, int W
     cur = ll;
     cur_pitch = ll_pitch;
   }
+  // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
+  // level l wrote last, which are the likeliest still in L2 (LL uses normal
+  // stores, the detail bands evict-first). The level pair writes LL_2
+  // top-down, like a forward-order level.
+  bool reverse = false;
   for (int l = 1; l <= levels; ++l) {
     if (l == 1 && levels >= 2 && launch_pair(p, lv[0], lv[1], st)) {
       if (events) record(events[1], st), record(events[2], st);
       ++l;
+      reverse = true;
       continue;
     }
     gpu::LevelArgs a = lv[l - 1];
-    // Alternate the chunk order: level l + 1 starts on the rows of LL_l that
-    // level l wrote last, which are still in L2 (LL uses normal stores, the
-    // detail bands evict-first).
-    a.reverse = (l % 2 == 0) ? 1 : 0;
+    a.reverse = reverse ? 1 : 0;
+    reverse = !reverse;
     launch(p, a, kFromImage, st);
     if (events) record(events[l], st);
   }
