@@ -92,6 +92,10 @@ typedef struct {
   int32_t extension;       /* dwt2d_extension */
   int32_t forward;         /* 1 forward analysis, 0 inverse synthesis */
   int32_t fused_multiply_add; /* 0: round(w*v) then add (reference arithmetic), 1: fma per tap */
+  /* optional float64 tables for compile<double>: ntaps weights and nsteps*4
+   * row scales in double precision (NULL: the plan has no float64 path) */
+  const double* weights64;
+  const double* scales64;
 } dwt2d_program;
 
 typedef struct dwt2d_plan dwt2d_plan;
@@ -268,6 +272,29 @@ DWT2D_B200_API int dwt2d_forward_mallat_sharded(const dwt2d_plan* plan, int nran
                                                 const float* const* strips, const size_t* pitch, int width,
                                                 int strip_height, int levels, float* const* out,
                                                 const size_t* out_pitch, void* const* streams);
+
+/* --- float64 execution (compile<double> / run<double>, executor.hpp:52-238) --
+ * The reference's executor is a template; its float64 instance (the
+ * precision of its `equiv` harness, equiv.cpp:161-168) runs here on the
+ * GPU's generic executor: one pass per sub-step, the plan's taps with
+ * double weights (T)(coef * pre) and scales (T)post, the same tap order and
+ * rounding model as the float32 path (composed programs: product rounded,
+ * then the sum — bit-identical to the reference's run<double>). Periodic
+ * and symmetric extension. Plans from dwt2d_plan_create always carry the
+ * float64 tables; plans from dwt2d_plan_create_from_program only with
+ * weights64/scales64 (else DWT2D_EUNSUPPORTED). */
+DWT2D_B200_API int dwt2d_run_planar_f64(const dwt2d_plan* plan, const double* const in[4],
+                                        const size_t in_pitch[4], double* const out[4],
+                                        const size_t out_pitch[4], int w2, int h2, void* stream);
+DWT2D_B200_API int dwt2d_forward_level_f64(const dwt2d_plan* plan, const double* image, size_t pitch,
+                                           int width, int height, double* const out[4],
+                                           const size_t out_pitch[4], void* stream);
+DWT2D_B200_API int dwt2d_inverse_level_f64(const dwt2d_plan* plan, const double* const in[4],
+                                           const size_t in_pitch[4], double* image, size_t pitch,
+                                           int width, int height, void* stream);
+/* run<double> on host planes (H2D, the passes, D2H; returns when done) */
+DWT2D_B200_API int dwt2d_run_planar_host_f64(const dwt2d_plan* plan, const double* const in[4],
+                                             double* const out[4], int w2, int h2);
 
 /* --- multi-level (Mallat pyramid), device buffers --------
  * Layout: after level l the top-left w x h LL region is replaced by

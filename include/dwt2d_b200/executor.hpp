@@ -9,8 +9,11 @@
 // the ahead-of-time sm_100a kernel whose tables have the same fingerprint.
 //
 // Differences a caller can see:
-//  * T must be float — the GPU path computes in float32 (the north-star
-//    precision); ExecPlan<double> is rejected at compile time.
+//  * T is float or double. float runs the fused sm_100a kernels; double
+//    (the reference's equiv precision) runs the generic GPU executor with
+//    float64 weights and scales (dwt2d_run_planar_host_f64), one pass per
+//    sub-step, composed programs bit-identical to the reference's
+//    run<double>.
 //  * `workers` is validated (>= 1) and recorded but does not change the
 //    result or the launch; the reference's worker bit-identity holds
 //    trivially.
@@ -46,8 +49,8 @@ struct PlanDeleter {
 
 template <typename T>
 struct ExecPlan {
-  static_assert(std::is_same_v<T, float>,
-                "dwt2d_b200 runs the transform in float32 on the GPU: use ExecPlan<float>");
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>,
+                "dwt2d_b200 runs the transform in float32 or float64: use ExecPlan<float> or ExecPlan<double>");
   std::shared_ptr<dwt2d_plan> handle;  // null for a scheme without steps
   Extension extension = Extension::periodic;
   int worker_count = 1;
@@ -67,15 +70,20 @@ ExecPlan<T> compile(const Scheme& s, Extension ext, int workers) {
   const StepProgram prog = lower(s, default_lowering(s));
   std::vector<dwt2d_row> rows;
   std::vector<dwt2d_tap> taps;
+  std::vector<double> w64, s64;  // compile<double>: (T)(coef * pre), (T)post
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) {
       dwt2d_row row{};
       row.identity = r.identity;
       row.scale = r.scale;
       row.tap_begin = int32_t(taps.size());
-      for (const KernelTap& k : r.taps) taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+      for (const KernelTap& k : r.taps) {
+        taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+        w64.push_back(k.coef);
+      }
       row.tap_end = int32_t(taps.size());
       rows.push_back(row);
+      s64.push_back(r.scale64);
     }
   dwt2d_program t{};
   t.nsteps = int32_t(prog.steps.size());
@@ -86,6 +94,7 @@ ExecPlan<T> compile(const Scheme& s, Extension ext, int workers) {
   t.extension = ext == Extension::periodic ? DWT2D_PERIODIC : DWT2D_SYMMETRIC;
   t.forward = s.kind != SchemeKind::inverse_lifting;
   t.fused_multiply_add = prog.fused_multiply_add;
+  if constexpr (std::is_same_v<T, double>) t.weights64 = w64.data(), t.scales64 = s64.data();
   dwt2d_plan* raw = nullptr;
   detail::throw_status(dwt2d_plan_create_from_program(&t, &raw));
   plan.handle.reset(raw, detail::PlanDeleter{});
@@ -104,14 +113,17 @@ PolyphaseImage<T> run(ExecPlan<T>& plan, const PolyphaseImage<T>& in) {
   if (!plan.handle) return in;
   PolyphaseImage<T> out;
   out.extension = in.extension;
-  const float* src[4];
-  float* dst[4];
+  const T* src[4];
+  T* dst[4];
   for (int j = 0; j < 4; ++j) {
     out.comp[j] = ImagePlane<T>(w2, h2);
     src[j] = in.comp[j].samples.data();
     dst[j] = out.comp[j].samples.data();
   }
-  detail::throw_status(dwt2d_run_planar_host(plan.handle.get(), src, dst, w2, h2));
+  if constexpr (std::is_same_v<T, double>)
+    detail::throw_status(dwt2d_run_planar_host_f64(plan.handle.get(), src, dst, w2, h2));
+  else
+    detail::throw_status(dwt2d_run_planar_host(plan.handle.get(), src, dst, w2, h2));
   plan.barrier_count = plan.logical_steps;
   return out;
 }

@@ -38,6 +38,7 @@ struct KernelTap {
 struct KernelRow {
   bool identity = false;  // output component == input component
   float scale = 1.0f;     // applied after accumulation (post-scale)
+  double scale64 = 1.0;   // the same post-scale for float64 execution (compile<double>)
   std::vector<KernelTap> taps;
 };
 

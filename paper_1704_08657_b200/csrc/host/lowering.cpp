@@ -27,6 +27,7 @@ KernelStep lower_matrix(const PolyMatrix& m, const std::array<double, 4>& pre,
       continue;
     }
     row.scale = static_cast<float>(post[r]);
+    row.scale64 = post[r];
     for (int j = 0; j < 4; ++j) {
       std::vector<Term> t = m.at(r, j).terms();
       std::sort(t.begin(), t.end(), [](const Term& a, const Term& b) {

@@ -83,7 +83,49 @@ __global__ void __launch_bounds__(256) generic_step_kernel(const __grid_constant
   }
 }
 
+// float64 (compile<double>): one sub-step over one grid; tiles of 32 x 8
+__global__ void __launch_bounds__(256) generic_step64_kernel(const __grid_constant__ GenericStepArgs64 a) {
+  const int tiles_x = (a.w2 + 31) / 32;
+  const int x = (int(blockIdx.x) % tiles_x) * 32 + threadIdx.x;
+  const int y = (int(blockIdx.x) / tiles_x) * 8 + threadIdx.y;
+  if (x < a.kx0 || x >= a.kx1 || y < a.ky0 || y >= a.ky1) return;
+  auto load = [&](int j, int xx, int yy) {
+    if (a.in_il) return a.in[0][(2ll * yy + (j >> 1)) * a.in_pitch[0] + 2ll * xx + (j & 1)];
+    return a.in[j][(long long)yy * a.in_pitch[j] + xx];
+  };
+  for (int r = 0; r < 4; ++r) {
+    double v;
+    if (a.rows[r].ident) {
+      v = load(r, x, y);
+    } else {
+      double acc = 0.0;
+      for (int t = a.rows[r].tb; t < a.rows[r].te; ++t) {
+        const TapDesc64 tp = a.taps[t];
+        const double s = load(tp.j, extend(x + tp.dm, a.w2, a.symmetric), extend(y + tp.dn, a.h2, a.symmetric));
+        if (t == a.rows[r].tb)
+          acc = tp.w == 1.0 ? s : __dmul_rn(tp.w, s);
+        else if (a.fma)
+          acc = __fma_rn(tp.w, s, acc);
+        else
+          acc = __dadd_rn(acc, tp.w == 1.0 ? s : __dmul_rn(tp.w, s));
+      }
+      v = a.rows[r].scale == 1.0 ? acc : __dmul_rn(acc, a.rows[r].scale);
+    }
+    if (a.out_il)
+      a.out[0][(2ll * y + (r >> 1)) * a.out_pitch[0] + 2ll * x + (r & 1)] = v;
+    else
+      a.out[r][(long long)y * a.out_pitch[r] + x] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_generic_step64(const GenericStepArgs64& a, cudaStream_t st) {
+  const long long tiles = (long long)((a.w2 + 31) / 32) * ((a.h2 + 7) / 8);
+  if (tiles <= 0) return cudaSuccess;
+  generic_step64_kernel<<<unsigned(tiles), dim3(32, 8), 0, st>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_generic_step(const GenericStepArgs* a, int n, bool pdl, cudaStream_t st) {
   if (n < 1 || n > kMaxGenericRegions) return cudaErrorInvalidValue;

@@ -153,6 +153,32 @@ struct CropTileArgs {
 
 cudaError_t launch_crop_tiles(const CropTileArgs& a, int smem_floats, bool pdl, cudaStream_t st);
 
+// The generic executor in float64 (compile<double>): the same pass with
+// double data, weights and scales.
+struct TapDesc64 {
+  int j, dm, dn;
+  double w;
+};
+struct RowDesc64 {
+  int ident, tb, te;
+  double scale;
+};
+struct GenericStepArgs64 {
+  const double* in[4];
+  long long in_pitch[4];
+  int in_il;
+  double* out[4];
+  long long out_pitch[4];
+  int out_il;
+  int w2, h2;
+  int symmetric;
+  int fma;
+  int kx0, kx1, ky0, ky1;
+  RowDesc64 rows[4];
+  const TapDesc64* taps;
+};
+cudaError_t launch_generic_step64(const GenericStepArgs64& a, cudaStream_t st);
+
 // up to kMaxGenericRegions independent passes (same sub-step, different
 // grids) in one launch
 constexpr int kMaxGenericRegions = 4;

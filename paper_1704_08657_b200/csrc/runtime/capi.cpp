@@ -91,6 +91,14 @@ struct dwt2d_plan {
   };
   mutable std::mutex dev_mu;
   mutable DeviceTables dev[kMaxDevices];
+  // float64 execution (compile<double>): double weights and row scales of
+  // the same tables, uploaded per device on first use
+  bool has64 = false;
+  std::vector<double> w64, scale64;
+  struct DeviceTables64 {
+    gpu::TapDesc64* taps = nullptr;
+  };
+  mutable DeviceTables64 dev64[kMaxDevices];
   // rings of shards of dwt2d_forward_mallat_sharded, one per geometry
   struct ShardRing {
     std::vector<long long> key;
@@ -104,6 +112,8 @@ struct dwt2d_plan {
       if (d.taps) cudaFree(d.taps);
       if (d.rows) cudaFree(d.rows);
     }
+    for (DeviceTables64& d : dev64)
+      if (d.taps) cudaFree(d.taps);
   }
 };
 
@@ -430,6 +440,88 @@ void run_generic(const dwt2d_plan& p, const gpu::LevelArgs& a, Layout layout, cu
 
 void launch_fused(const dwt2d_plan& p, gpu::LevelArgs a, Layout layout, cudaStream_t st);
 
+// float64 tap table of the plan on the current device
+const gpu::TapDesc64* device_taps64(const dwt2d_plan& p) {
+  if (!p.has64) fail(DWT2D_EUNSUPPORTED, "plan has no float64 tables (create it with float64 weights)");
+  const int devno = current_device();
+  std::lock_guard<std::mutex> lk(p.dev_mu);
+  dwt2d_plan::DeviceTables64& dt = p.dev64[devno];
+  if (!dt.taps) {
+    std::vector<gpu::TapDesc64> t;
+    for (size_t i = 0; i < p.taps.size(); ++i) t.push_back(gpu::TapDesc64{p.taps[i].comp, p.taps[i].dm, p.taps[i].dn, p.w64[i]});
+    if (t.empty()) t.push_back(gpu::TapDesc64{0, 0, 0, 0.0});
+    gpu::TapDesc64* d = nullptr;
+    cuda_check(cudaMalloc(&d, t.size() * sizeof(gpu::TapDesc64)), "tap table allocation");
+    cuda_check(cudaMemcpy(d, t.data(), t.size() * sizeof(gpu::TapDesc64), cudaMemcpyHostToDevice), "tap table upload");
+    dt.taps = d;
+  }
+  return dt.taps;
+}
+
+// One level in float64 (compile<double> + run<double>): one generic pass
+// per sub-step over double planes, double-buffered temporaries from the
+// stream-ordered allocator (the reference's run() loop, executor.hpp:196-238).
+struct Level64 {
+  const double* in[4];
+  size_t in_pitch[4];
+  double* out[4];
+  size_t out_pitch[4];
+};
+void run_level64(const dwt2d_plan& p, const Level64& lv, Layout layout, int w2, int h2, cudaStream_t st) {
+  if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+  const gpu::TapDesc64* taps = device_taps64(p);
+  const int S = p.substeps;
+  const size_t plane = ws_align(size_t(w2) * size_t(h2));
+  double* tmp = nullptr;
+  if (S > 1) {
+    void* m = nullptr;
+    cuda_check(cudaMallocAsync(&m, 8 * plane * sizeof(double), st), "float64 temporaries");
+    tmp = static_cast<double*>(m);
+  }
+  for (int s = 0; s < S; ++s) {
+    const bool first = s == 0, last = s == S - 1;
+    double* src_tmp = tmp ? tmp + size_t((s + 1) % 2) * 4 * plane : nullptr;
+    double* dst_tmp = tmp ? tmp + size_t(s % 2) * 4 * plane : nullptr;
+    gpu::GenericStepArgs64 q{};
+    for (int j = 0; j < 4; ++j) {
+      if (first) {
+        q.in[j] = lv.in[layout == kFromImage ? 0 : j];
+        q.in_pitch[j] = (long long)lv.in_pitch[layout == kFromImage ? 0 : j];
+      } else {
+        q.in[j] = src_tmp + j * plane;
+        q.in_pitch[j] = w2;
+      }
+      if (last) {
+        q.out[j] = lv.out[layout == kToImage ? 0 : j];
+        q.out_pitch[j] = (long long)lv.out_pitch[layout == kToImage ? 0 : j];
+      } else {
+        q.out[j] = dst_tmp + j * plane;
+        q.out_pitch[j] = w2;
+      }
+      const dwt2d_row& row = p.rows[size_t(s) * 4 + j];
+      q.rows[j] = gpu::RowDesc64{row.identity, row.tap_begin, row.tap_end, p.scale64[size_t(s) * 4 + j]};
+    }
+    q.in_il = first && layout == kFromImage;
+    q.out_il = last && layout == kToImage;
+    q.w2 = w2, q.h2 = h2;
+    q.symmetric = p.extension == DWT2D_SYMMETRIC;
+    q.fma = p.fma;
+    q.kx0 = 0, q.kx1 = w2, q.ky0 = 0, q.ky1 = h2;
+    q.taps = taps;
+    cuda_check(gpu::launch_generic_step64(q, st), "float64 step launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  if (tmp) cuda_check(cudaFreeAsync(tmp, st), "float64 temporaries");
+}
+
+void copy_planes64(const double* const in[4], const size_t in_pitch[4], double* const out[4],
+                   const size_t out_pitch[4], int w2, int h2, cudaStream_t st) {
+  for (int j = 0; j < 4; ++j)
+    cuda_check(cudaMemcpy2DAsync(out[j], out_pitch[j] * 8, in[j], in_pitch[j] * 8, size_t(w2) * 8, h2,
+                                 cudaMemcpyDeviceToDevice, st),
+               "copy");
+}
+
 // Symmetric extension with a fused kernel. The extension
 // only matters for outputs whose dependency cone — the level's reach, up/down
 // rows and left/right columns over all sub-steps — crosses the image edge;
@@ -651,16 +743,20 @@ void finalize_plan(dwt2d_plan& p, const StepProgram& prog, int extension) {
   p.extension = extension;
   p.fma = prog.fused_multiply_add ? 1 : 0;
   p.tune = tuning_from_env();
-  p.rows.clear(), p.taps.clear();
+  p.rows.clear(), p.taps.clear(), p.w64.clear(), p.scale64.clear();
   for (const KernelStep& st : prog.steps)
     for (const KernelRow& r : st.rows) {
       dwt2d_row row{};
       row.identity = r.identity;
       row.scale = r.scale;
       row.tap_begin = int32_t(p.taps.size());
-      for (const KernelTap& k : r.taps) p.taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+      for (const KernelTap& k : r.taps) {
+        p.taps.push_back(dwt2d_tap{k.comp, k.dm, k.dn, k.w});
+        p.w64.push_back(k.coef);
+      }
       row.tap_end = int32_t(p.taps.size());
       p.rows.push_back(row);
+      p.scale64.push_back(r.scale64);
     }
   bool identity = true;
   for (const KernelStep& st : prog.steps)
@@ -690,13 +786,14 @@ StepProgram program_from_tables(const dwt2d_program& t) {
       KernelRow& kr = st.rows[r];
       kr.identity = row.identity != 0;
       kr.scale = row.scale;
+      kr.scale64 = t.scales64 ? t.scales64[s * 4 + r] : row.scale;
       if (row.tap_begin < 0 || row.tap_end > t.ntaps || row.tap_begin > row.tap_end)
         fail(DWT2D_EINVAL, "malformed program tap range");
       for (int i = row.tap_begin; i < row.tap_end; ++i) {
         const dwt2d_tap& tp = t.taps[i];
         if (tp.comp < 0 || tp.comp > 3) fail(DWT2D_EINVAL, "malformed program tap component");
         KernelTap k;
-        k.comp = tp.comp, k.dm = tp.dm, k.dn = tp.dn, k.w = tp.w, k.coef = tp.w;
+        k.comp = tp.comp, k.dm = tp.dm, k.dn = tp.dn, k.w = tp.w, k.coef = t.weights64 ? t.weights64[i] : tp.w;
         kr.taps.push_back(k);
         st.min_dm = std::min(st.min_dm, k.dm), st.max_dm = std::max(st.max_dm, k.dm);
         st.min_dn = std::min(st.min_dn, k.dn), st.max_dn = std::max(st.max_dn, k.dn);
@@ -1474,6 +1571,7 @@ int dwt2d_plan_create(const dwt2d_plan_desc* d, dwt2d_plan** out) {
     p->operations = count_operations(s);
     p->description = describe(s);
     finalize_plan(*p, prog, d->extension);
+    p->has64 = true;
     *out = p.release();
   });
 }
@@ -1486,6 +1584,7 @@ int dwt2d_plan_create_from_program(const dwt2d_program* t, dwt2d_plan** out) {
     auto p = std::make_unique<dwt2d_plan>();
     p->forward = t->forward != 0;
     finalize_plan(*p, prog, t->extension);
+    p->has64 = t->weights64 != nullptr;
     if (p->entry) p->key = p->entry->key;
     *out = p.release();
   });
@@ -1901,6 +2000,76 @@ int dwt2d_run_planar_host(const dwt2d_plan* p, const float* const in[4], float* 
     }
     for (int j = 0; j < 4; ++j)
       cuda_check(cudaMemcpyAsync(out[j], dout[j], n * 4, cudaMemcpyDeviceToHost, hp.comp), "D2H");
+    cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
+  });
+}
+
+// ------------------------------------------------ float64 (C ABI)
+
+int dwt2d_run_planar_f64(const dwt2d_plan* p, const double* const in[4], const size_t in_pitch[4],
+                         double* const out[4], const size_t out_pitch[4], int w2, int h2, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!in || !out || !in_pitch || !out_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    for (int j = 0; j < 4; ++j)
+      if (in_pitch[j] < size_t(w2) || out_pitch[j] < size_t(w2)) fail(DWT2D_EINVAL, "pitch < width");
+    if (is_identity(*p)) return copy_planes64(in, in_pitch, out, out_pitch, w2, h2, as_stream(stream));
+    Level64 lv{};
+    for (int j = 0; j < 4; ++j)
+      lv.in[j] = in[j], lv.in_pitch[j] = in_pitch[j], lv.out[j] = out[j], lv.out_pitch[j] = out_pitch[j];
+    run_level64(*p, lv, kPlanar, w2, h2, as_stream(stream));
+  });
+}
+
+int dwt2d_forward_level_f64(const dwt2d_plan* p, const double* image, size_t pitch, int width, int height,
+                            double* const out[4], const size_t out_pitch[4], void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!image || !out || !out_pitch) fail(DWT2D_EINVAL, "null argument");
+    if (!p->forward) fail(DWT2D_EINVAL, "forward_level: plan is an inverse plan");
+    if (width <= 0 || height <= 0 || width % 2 || height % 2) fail(DWT2D_EINVAL, "image sides must be positive and even");
+    if (pitch < size_t(width)) fail(DWT2D_EINVAL, "pitch < width");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    Level64 lv{};
+    for (int j = 0; j < 4; ++j) lv.in[j] = image, lv.in_pitch[j] = pitch, lv.out[j] = out[j], lv.out_pitch[j] = out_pitch[j];
+    run_level64(*p, lv, kFromImage, width / 2, height / 2, as_stream(stream));
+  });
+}
+
+int dwt2d_inverse_level_f64(const dwt2d_plan* p, const double* const in[4], const size_t in_pitch[4], double* image,
+                            size_t pitch, int width, int height, void* stream) {
+  return guard([&] {
+    require_plan(p);
+    if (!in || !in_pitch || !image) fail(DWT2D_EINVAL, "null argument");
+    if (p->forward) fail(DWT2D_EINVAL, "inverse_level: plan is not an inverse plan");
+    if (width <= 0 || height <= 0 || width % 2 || height % 2) fail(DWT2D_EINVAL, "image sides must be positive and even");
+    if (pitch < size_t(width)) fail(DWT2D_EINVAL, "pitch < width");
+    if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
+    Level64 lv{};
+    for (int j = 0; j < 4; ++j) lv.in[j] = in[j], lv.in_pitch[j] = in_pitch[j], lv.out[j] = image, lv.out_pitch[j] = pitch;
+    run_level64(*p, lv, kToImage, width / 2, height / 2, as_stream(stream));
+  });
+}
+
+int dwt2d_run_planar_host_f64(const dwt2d_plan* p, const double* const in[4], double* const out[4], int w2, int h2) {
+  return guard([&] {
+    require_plan(p);
+    if (!in || !out) fail(DWT2D_EINVAL, "null argument");
+    if (w2 <= 0 || h2 <= 0) fail(DWT2D_EINVAL, "run: empty input");
+    HostPipe& hp = host_pipe();
+    const size_t n = size_t(w2) * h2;
+    double* dev = static_cast<double*>(hp.reserve(8 * n * sizeof(double)));
+    Level64 lv{};
+    for (int j = 0; j < 4; ++j) {
+      lv.in[j] = dev + j * n, lv.out[j] = dev + (4 + j) * n;
+      lv.in_pitch[j] = lv.out_pitch[j] = size_t(w2);
+      cuda_check(cudaMemcpyAsync(dev + j * n, in[j], n * 8, cudaMemcpyHostToDevice, hp.comp), "H2D");
+    }
+    if (is_identity(*p)) copy_planes64(lv.in, lv.in_pitch, lv.out, lv.out_pitch, w2, h2, hp.comp);
+    else run_level64(*p, lv, kPlanar, w2, h2, hp.comp);
+    for (int j = 0; j < 4; ++j)
+      cuda_check(cudaMemcpyAsync(out[j], lv.out[j], n * 8, cudaMemcpyDeviceToHost, hp.comp), "D2H");
     cuda_check(cudaStreamSynchronize(hp.comp), "synchronize");
   });
 }

@@ -54,7 +54,8 @@ class Program(ctypes.Structure):
     _fields_ = [("nsteps", ctypes.c_int32), ("rows", ctypes.POINTER(Row)), ("ntaps", ctypes.c_int32),
                 ("taps", ctypes.POINTER(Tap)), ("logical_steps", ctypes.c_int32),
                 ("extension", ctypes.c_int32), ("forward", ctypes.c_int32),
-                ("fused_multiply_add", ctypes.c_int32)]
+                ("fused_multiply_add", ctypes.c_int32),
+                ("weights64", ctypes.POINTER(ctypes.c_double)), ("scales64", ctypes.POINTER(ctypes.c_double))]
 
 
 class PlanInfo(ctypes.Structure):
@@ -130,6 +131,10 @@ _SIGS = {
     "dwt2d_inverse_mallat": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p, _sz,
                                             _p, _p]),
     "dwt2d_run_planar_host": (ctypes.c_int, [_p, _P4, _P4, ctypes.c_int, ctypes.c_int]),
+    "dwt2d_run_planar_f64": (ctypes.c_int, [_p, _P4, _S4, _P4, _S4, ctypes.c_int, ctypes.c_int, _p]),
+    "dwt2d_forward_level_f64": (ctypes.c_int, [_p, _p, _sz, ctypes.c_int, ctypes.c_int, _P4, _S4, _p]),
+    "dwt2d_inverse_level_f64": (ctypes.c_int, [_p, _P4, _S4, _p, _sz, ctypes.c_int, ctypes.c_int, _p]),
+    "dwt2d_run_planar_host_f64": (ctypes.c_int, [_p, _P4, _P4, ctypes.c_int, ctypes.c_int]),
     "dwt2d_forward_mallat_host": (ctypes.c_int, [_p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p]),
     "dwt2d_inverse_mallat_host": (ctypes.c_int, [_p, _p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _p]),
     "dwt2d_time_forward": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,

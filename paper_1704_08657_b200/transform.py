@@ -26,10 +26,11 @@ def _stream_handle(stream) -> int | None:
     return stream.cuda_stream
 
 
-def _dev(t, name="tensor"):
+def _dev(t, name="tensor", dtype=None):
     import torch
-    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
-        raise TypeError(f"{name} must be a float32 CUDA tensor")
+    dtype = dtype or torch.float32
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype:
+        raise TypeError(f"{name} must be a {str(dtype).replace('torch.', '')} CUDA tensor")
     if t.dim() != 2 or (t.size(1) > 1 and t.stride(1) != 1):
         raise ValueError(f"{name} must be 2-D with unit column stride")
     return t.data_ptr(), (t.stride(0) if t.size(0) > 1 else t.size(1))
@@ -130,38 +131,44 @@ class Plan:
 
     # -- device tensors ------------------------------------------------
     def run(self, planes: Sequence, out: Sequence | None = None, stream=None):
-        """run<float> on four [h2, w2] CUDA tensors (ee, oe, eo, oo)."""
+        """run<T> on four [h2, w2] CUDA tensors (ee, oe, eo, oo): float32
+        planes run the fused kernels, float64 planes the float64 executor
+        (compile<double>, dwt2d_run_planar_f64)."""
         import torch
         h2, w2 = planes[0].shape
+        dt = planes[0].dtype if planes[0].dtype == torch.float64 else torch.float32
         if out is None:
-            out = [torch.empty((h2, w2), dtype=torch.float32, device=planes[0].device) for _ in range(4)]
-        ip, op = zip(*[_dev(p, "plane") for p in planes]), zip(*[_dev(o, "out") for o in out])
+            out = [torch.empty((h2, w2), dtype=dt, device=planes[0].device) for _ in range(4)]
+        ip, op = zip(*[_dev(p, "plane", dt) for p in planes]), zip(*[_dev(o, "out", dt) for o in out])
         iptr, ipit = list(ip)
         optr, opit = list(op)
-        N.check(N.lib.dwt2d_run_planar(self._h, N._P4(*iptr), N._S4(*ipit), N._P4(*optr), N._S4(*opit),
-                                       w2, h2, _stream_handle(stream)))
+        fn = N.lib.dwt2d_run_planar_f64 if dt == torch.float64 else N.lib.dwt2d_run_planar
+        N.check(fn(self._h, N._P4(*iptr), N._S4(*ipit), N._P4(*optr), N._S4(*opit), w2, h2, _stream_handle(stream)))
         return list(out)
 
     def forward_level(self, image, out: Sequence | None = None, stream=None):
+        """One forward level of a float32 (fused kernels) or float64 image."""
         import torch
         H, W = image.shape
+        dt = image.dtype if image.dtype == torch.float64 else torch.float32
         if out is None:
-            out = [torch.empty((H // 2, W // 2), dtype=torch.float32, device=image.device) for _ in range(4)]
-        ptr, pitch = _dev(image, "image")
-        optr, opit = zip(*[_dev(o, "out") for o in out])
-        N.check(N.lib.dwt2d_forward_level(self._h, ptr, pitch, W, H, N._P4(*optr), N._S4(*opit),
-                                          _stream_handle(stream)))
+            out = [torch.empty((H // 2, W // 2), dtype=dt, device=image.device) for _ in range(4)]
+        ptr, pitch = _dev(image, "image", dt)
+        optr, opit = zip(*[_dev(o, "out", dt) for o in out])
+        fn = N.lib.dwt2d_forward_level_f64 if dt == torch.float64 else N.lib.dwt2d_forward_level
+        N.check(fn(self._h, ptr, pitch, W, H, N._P4(*optr), N._S4(*opit), _stream_handle(stream)))
         return list(out)
 
     def inverse_level(self, planes: Sequence, image=None, stream=None):
         import torch
         h2, w2 = planes[0].shape
+        dt = planes[0].dtype if planes[0].dtype == torch.float64 else torch.float32
         if image is None:
-            image = torch.empty((2 * h2, 2 * w2), dtype=torch.float32, device=planes[0].device)
-        iptr, ipit = zip(*[_dev(p, "plane") for p in planes])
-        ptr, pitch = _dev(image, "image")
-        N.check(N.lib.dwt2d_inverse_level(self._h, N._P4(*iptr), N._S4(*ipit), ptr, pitch, 2 * w2, 2 * h2,
-                                          _stream_handle(stream)))
+            image = torch.empty((2 * h2, 2 * w2), dtype=dt, device=planes[0].device)
+        iptr, ipit = zip(*[_dev(p, "plane", dt) for p in planes])
+        ptr, pitch = _dev(image, "image", dt)
+        fn = N.lib.dwt2d_inverse_level_f64 if dt == torch.float64 else N.lib.dwt2d_inverse_level
+        N.check(fn(self._h, N._P4(*iptr), N._S4(*ipit), ptr, pitch, 2 * w2, 2 * h2, _stream_handle(stream)))
         return image
 
     def forward_level_strip(self, strip, top, bottom, out: Sequence | None = None, stream=None):

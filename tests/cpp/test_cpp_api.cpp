@@ -223,6 +223,34 @@ void gpu_tests() {
     const auto out = run(plan, in);
     CHECK(out == in);
   }
+  // compile<double> / run<double>: the float64 executor agrees with the
+  // float32 transform to float32 precision and round-trips to 1e-12, for
+  // both extensions (the reference's equiv precision, equiv.cpp:161-168)
+  for (Extension ext : {Extension::periodic, Extension::symmetric}) {
+    const WaveletSpec w = get_wavelet("cdf97");
+    const auto imgd = random_image<double>(64, 48, 404);
+    const auto ind = polyphase_split(imgd, ext);
+    const auto inf = polyphase_split(random_image<float>(64, 48, 404), ext);
+    for (bool optimize : {false, true}) {
+      Scheme s = build_scheme(SchemeKind::nonseparable_lifting, w);
+      if (optimize) s = optimize_constant_split(s, w);
+      ExecPlan<double> pd = compile<double>(s, ext, 2);
+      ExecPlan<float> pf = compile<float>(s, ext, 2);
+      const auto od = run(pd, ind);
+      const auto of = run(pf, inf);
+      double m = 0;
+      for (int j = 0; j < 4; ++j)
+        for (size_t i = 0; i < od.comp[j].samples.size(); ++i)
+          m = std::max(m, std::abs(od.comp[j].samples[i] - double(of.comp[j].samples[i])));
+      CHECK(m < 2e-5);
+      const auto back = inverse_lifting(w, od, 1);
+      double e = 0;
+      for (int j = 0; j < 4; ++j)
+        for (size_t i = 0; i < back.comp[j].samples.size(); ++i)
+          e = std::max(e, std::abs(back.comp[j].samples[i] - ind.comp[j].samples[i]));
+      CHECK(e < 1e-12);
+    }
+  }
   // input validation (test_executor.cpp:343-355)
   {
     auto plan = compile<float>(build_separable_lifting(get_wavelet("cdf53")), Extension::periodic, 1);
