@@ -6,19 +6,21 @@
 //
 //   dwt2d describe  --wavelet W --scheme S [--optimize]
 //   dwt2d count     --wavelet W
-//   dwt2d equiv     --wavelet W --size N --seed K --extension E
+//   dwt2d equiv     --wavelet W --size N --seed K --extension E [--precision 64|32]
 //   dwt2d transform in.pgm --out DIR [--wavelet --scheme --optimize
-//                   --extension --precision 32 --workers N --levels L]
+//                   --extension --precision 64|32 --workers N --levels L]
 //   dwt2d bench     [--wavelet --scheme all|ID --optimize --sizes a,b,..
 //                   --workers --repeats --precision 32 --seed --extension
 //                   --levels L --out FILE]
 //
-// Differences: transforms run on the GPU in float32 (--precision 64 is a
-// usage error); `equiv` compares the GPU float32 outputs of all ten variants
-// (tolerance 1e-5 relative, the float32 parity bar, instead of the
-// reference's double-precision 1e-12/1e-9); `transform --levels L` writes a
-// Mallat pyramid as DIR/level<l>/ sub-band sets; `bench --levels L` times
-// the pyramid.
+// Precision: like the reference, `transform` and `equiv` default to float64
+// (the GPU's float64 executor: compile<double>/run<double>, one pass per
+// sub-step) and take --precision 32 for the fused float32 kernels; `equiv`
+// in float64 uses the reference's tolerance (1e-12 with exact coefficients,
+// else 1e-9, equiv.cpp:34-47), in float32 the float32 parity bar 1e-5.
+// `bench` times the float32 kernels only (--precision 64 is a usage error).
+// Additions: `transform --levels L` writes a Mallat pyramid as
+// DIR/level<l>/ sub-band sets; `bench --levels L` times the pyramid.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -58,9 +60,9 @@ const char* kUsage =
     "usage: dwt2d <describe|count|equiv|transform|bench> [options]\n"
     "  describe  --wavelet W --scheme S [--optimize]\n"
     "  count     --wavelet W\n"
-    "  equiv     --wavelet W --size N --seed K --extension periodic|symmetric\n"
+    "  equiv     --wavelet W --size N --seed K --extension periodic|symmetric --precision 64|32\n"
     "  transform IN.pgm --out DIR [--wavelet W --scheme S --optimize --extension E\n"
-    "            --precision 32 --workers N --levels L]\n"
+    "            --precision 64|32 --workers N --levels L]\n"
     "  bench     [--wavelet W --scheme all|S --optimize --sizes 256,512 --workers N\n"
     "            --repeats R --precision 32 --seed K --extension E --levels L --out FILE]\n";
 
@@ -119,10 +121,10 @@ Extension extension_of(const std::string& s) {
   throw Usage("unknown extension: " + s + " (valid: periodic symmetric)");
 }
 
-int precision_of(const Args& a, const char* def) {
+int precision_of(const Args& a, const char* def, bool allow64 = true) {
   const int p = to_int(a.get("--precision", def), "precision");
-  if (p == 64) throw Usage("precision 64 is not available: the GPU path computes in float32");
-  if (p != 32) throw Usage("precision must be 32 or 64");
+  if (p != 32 && p != 64) throw Usage("precision must be 32 or 64");
+  if (p == 64 && !allow64) throw Usage("bench: precision 64 is not timed (the float32 kernels are)");
   return p;
 }
 
@@ -155,7 +157,8 @@ int cmd_count(const Args& a) {
 }
 
 // max |a - b| / max(|a|, |b|) over the compared region (equiv.cpp:123-137)
-double rel_dev(const PolyphaseImage<float>& a, const PolyphaseImage<float>& b, int margin) {
+template <typename T>
+double rel_dev(const PolyphaseImage<T>& a, const PolyphaseImage<T>& b, int margin) {
   double mx = 0, md = 0;
   const int w2 = a.comp_width(), h2 = a.comp_height();
   for (int c = 0; c < 4; ++c)
@@ -168,22 +171,23 @@ double rel_dev(const PolyphaseImage<float>& a, const PolyphaseImage<float>& b, i
   return md / std::max(mx, 1e-300);
 }
 
-int cmd_equiv(const Args& a) {
-  allow(a, {"--wavelet", "--size", "--seed", "--extension"}, 0);
-  const WaveletSpec w = resolve_wavelet(a.get("--wavelet", "cdf53"));
-  const int size = to_int(a.get("--size", "64"), "size");
-  const int seed = to_int(a.get("--seed", "1"), "seed");
-  const std::string ext_s = a.get("--extension", "periodic");
+template <typename T>
+int equiv_at(const WaveletSpec& w, int size, int seed, const std::string& ext_s) {
   const Extension ext = extension_of(ext_s);
   const int margin = ext == Extension::symmetric ? 8 : 0;
-  const double tol = 1e-5;
-  const auto poly = polyphase_split(random_image<float>(size, size, std::uint64_t(seed)), ext);
-  std::vector<std::pair<std::string, PolyphaseImage<float>>> outs;
+  bool exact = true;  // equiv.cpp:34-38
+  for (const auto& pr : w.pairs()) {
+    for (const auto& t : pr.predict.terms()) exact = exact && t.c.is_exact();
+    for (const auto& t : pr.update.terms()) exact = exact && t.c.is_exact();
+  }
+  const double tol = std::is_same_v<T, double> ? (exact ? 1e-12 : 1e-9) : 1e-5;
+  const auto poly = polyphase_split(random_image<T>(size, size, std::uint64_t(seed)), ext);
+  std::vector<std::pair<std::string, PolyphaseImage<T>>> outs;
   for (SchemeKind k : all_scheme_kinds()) {
     const Scheme base = build_scheme(k, w);
     const Scheme opt = optimize_constant_split(base, w);
     for (const Scheme* s : {&base, &opt}) {
-      ExecPlan<float> plan = compile<float>(*s, ext, 1);
+      ExecPlan<T> plan = compile<T>(*s, ext, 1);
       outs.emplace_back(s->label, run(plan, poly));
     }
   }
@@ -196,18 +200,44 @@ int cmd_equiv(const Args& a) {
     }
   char buf[320];
   std::snprintf(buf, sizeof buf,
-                "equivalence wavelet=%s size=%d seed=%d extension=%s variants=%zu margin=%d device=B200-float32\n"
+                "equivalence wavelet=%s size=%d seed=%d extension=%s variants=%zu margin=%d device=B200-float%d\n"
                 "max relative deviation %.3e (tolerance %.0e)",
-                w.name().c_str(), size, seed, ext_s.c_str(), outs.size(), margin, worst, tol);
+                w.name().c_str(), size, seed, ext_s.c_str(), outs.size(), margin,
+                std::is_same_v<T, double> ? 64 : 32, worst, tol);
   std::cout << buf << (pair.empty() ? "" : " between " + pair) << (worst <= tol ? "\nPASS\n" : "\nFAIL\n");
   return worst <= tol ? 0 : 1;
+}
+
+int cmd_equiv(const Args& a) {
+  allow(a, {"--wavelet", "--size", "--seed", "--extension", "--precision"}, 0);
+  const WaveletSpec w = resolve_wavelet(a.get("--wavelet", "cdf53"));
+  const int size = to_int(a.get("--size", "64"), "size");
+  const int seed = to_int(a.get("--seed", "1"), "seed");
+  const std::string ext_s = a.get("--extension", "periodic");
+  extension_of(ext_s);
+  if (size <= 0 || size % 2) throw Usage("equiv: size must be positive and even");
+  return precision_of(a, "64") == 64 ? equiv_at<double>(w, size, seed, ext_s) : equiv_at<float>(w, size, seed, ext_s);
+}
+
+// transform_and_write (reference dwt2d.cpp:64-75), level after level
+template <typename T>
+void transform_levels(const ImagePlane<double>& img, const Scheme& s, Extension ext, int workers, int levels,
+                      const std::filesystem::path& out) {
+  ImagePlane<T> cur(img.width, img.height);
+  for (std::size_t i = 0; i < img.samples.size(); ++i) cur.samples[i] = static_cast<T>(img.samples[i]);
+  ExecPlan<T> plan = compile<T>(s, ext, workers);
+  for (int l = 1; l <= levels; ++l) {
+    const auto res = run(plan, polyphase_split(cur, ext));
+    write_subbands(res, levels == 1 ? out : out / ("level" + std::to_string(l)));
+    cur = res.comp[0];
+  }
 }
 
 int cmd_transform(const Args& a) {
   allow(a, {"--out", "--wavelet", "--scheme", "--optimize", "--extension", "--precision", "--workers", "--levels"}, 1);
   if (a.positional.empty()) throw Usage("transform: missing input PGM");
   if (!a.opt.count("--out")) throw Usage("transform: --out is required");
-  const int precision = precision_of(a, "32");
+  const int precision = precision_of(a, "64");  // the reference's default (dwt2d.cpp:121)
   const int workers = to_int(a.get("--workers", "1"), "workers");
   const int levels = to_int(a.get("--levels", "1"), "levels");
   if (levels < 1) throw Usage("levels must be at least 1");
@@ -216,14 +246,10 @@ int cmd_transform(const Args& a) {
                                a.has("--optimize"));
   const std::filesystem::path out = a.opt.at("--out");
   const ImagePlane<double> img = read_pgm(a.positional[0]);
-  ImagePlane<float> cur(img.width, img.height);
-  for (std::size_t i = 0; i < img.samples.size(); ++i) cur.samples[i] = float(img.samples[i]);
-  ExecPlan<float> plan = compile<float>(s, ext, workers);
-  for (int l = 1; l <= levels; ++l) {
-    const auto res = run(plan, polyphase_split(cur, ext));
-    write_subbands(res, levels == 1 ? out : out / ("level" + std::to_string(l)));
-    cur = res.comp[0];
-  }
+  if (precision == 64)
+    transform_levels<double>(img, s, ext, workers, levels, out);
+  else
+    transform_levels<float>(img, s, ext, workers, levels, out);
   std::cout << "wrote " << out.string() << (levels == 1 ? "" : "/level*") << "/{ee,oe,eo,oo}.raw: "
             << img.width / 2 << "x" << img.height / 2 << " per component, " << precision << "-bit, scheme "
             << s.label << ", wavelet " << s.wavelet << ", levels " << levels << ", device B200\n";
@@ -234,7 +260,7 @@ int cmd_bench(const Args& a) {
   allow(a, {"--wavelet", "--scheme", "--optimize", "--sizes", "--workers", "--repeats", "--precision", "--seed",
             "--extension", "--levels", "--out"},
         0);
-  const int precision = precision_of(a, "32");
+  const int precision = precision_of(a, "32", false);
   const int workers = to_int(a.get("--workers", "1"), "workers");
   const int repeats = to_int(a.get("--repeats", "3"), "repeats");
   const int seed = to_int(a.get("--seed", "1"), "seed");

@@ -58,12 +58,13 @@ def _write_pgm(path, img8):
     path.write_bytes(f"P5\n# test\n{w} {h}\n255\n".encode() + img8.astype(np.uint8).tobytes())
 
 
-def _read_subbands(d):
+def _read_subbands(d, precision="32"):
     out = []
     for lab in ["ee", "oe", "eo", "oo"]:
         hdr = dict(l.split() for l in (d / f"{lab}.hdr").read_text().splitlines() if l.strip())
-        assert hdr["precision"] == "32" and hdr["component"] == lab
-        a = np.fromfile(d / f"{lab}.raw", dtype="<f4").reshape(int(hdr["height"]), int(hdr["width"]))
+        assert hdr["precision"] == precision and hdr["component"] == lab
+        dt = "<f4" if precision == "32" else "<f8"
+        a = np.fromfile(d / f"{lab}.raw", dtype=dt).reshape(int(hdr["height"]), int(hdr["width"]))
         out.append(a)
     return out
 
@@ -74,6 +75,12 @@ def test_cli_equiv_passes_on_gpu():  # ctest cli_equiv
     assert "PASS" in r.stdout
     r = run("equiv", "--wavelet", "dd137", "--size", "64", "--extension", "symmetric", check=0)
     assert "PASS" in r.stdout
+    # float64 (the default) at the reference's tolerances, float32 at 1e-5
+    assert "device=B200-float64" in r.stdout and "tolerance 1e-12" in r.stdout
+    r = run("equiv", "--wavelet", "cdf97", "--size", "64", "--precision", "32", check=0)
+    assert "PASS" in r.stdout and "device=B200-float32" in r.stdout and "tolerance 1e-05" in r.stdout
+    r = run("equiv", "--wavelet", "cdf97", "--size", "64", check=0)
+    assert "PASS" in r.stdout and "tolerance 1e-09" in r.stdout
 
 
 @pytest.mark.gpu
@@ -83,11 +90,17 @@ def test_cli_transform_matches_oracle(tmp_path):
     pgm = tmp_path / "in.pgm"
     _write_pgm(pgm, img8)
     run("transform", pgm, "--out", tmp_path / "sb", "--wavelet", "cdf97", "--scheme", "nonseparable-lifting",
-        "--optimize", check=0)
+        "--optimize", "--precision", "32", check=0)
     got = _read_subbands(tmp_path / "sb")
     img = img8.astype(np.float64) / 255.0
     truth = O.transform("cdf97", "nonseparable-lifting", O.split(img.astype(np.float32).astype(np.float64)), True)
     assert max(float(np.max(np.abs(g - t))) for g, t in zip(got, truth)) <= 1e-5
+    # the reference's default precision: float64 (dwt2d.cpp:121)
+    run("transform", pgm, "--out", tmp_path / "sb64", "--wavelet", "cdf97", "--scheme", "nonseparable-lifting",
+        "--optimize", check=0)
+    got = _read_subbands(tmp_path / "sb64", "64")
+    truth = O.transform("cdf97", "nonseparable-lifting", O.split(img), True)
+    assert max(float(np.max(np.abs(g - t))) for g, t in zip(got, truth)) <= 1e-12
     run("transform", pgm, "--out", tmp_path / "pyr", "--levels", "3", check=0)
     assert (tmp_path / "pyr" / "level3" / "ee.raw").exists()
 
