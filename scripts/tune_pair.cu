@@ -114,6 +114,7 @@ int main(int argc, char** argv) {
     run("VF0 scalar", k_pair<0, 1>, 0);
     run("VF1 (c,c+1)", k_pair<1, 1>, 0);
     run("VF2 (c,c+2)", k_pair<2, 1>, 0);
+    run("VF1 minb3", k_pair<1, 3>, 0);
   }
   return 0;
 }
