@@ -200,12 +200,17 @@ def cpu_baseline_leg():
                                     f"one warm-up + median of 5 ({t1:.2f} s per pyramid)"}}
 
 
+REF_ARM_BUDGET_S = 75.0  # the whole --impl reference run, all steps and warm-ups
+
+
 def run_reference_arm(args, wl):
     """--impl reference: the reference's CPU path with every host thread, on
-    this arm's workload (rank 0 only). configs[3]: the whole 16384^2 image
-    per step; configs[4] (16 GiB image, more than the reference's ~4 copies
-    fit in host RAM): a declared 65536 x 2048 row band per step (the
-    reference's per-pixel rate)."""
+    this arm's workload (rank 0 only). Each step is one 8-level pyramid of a
+    row band of the workload's image (the metric is per pixel), as tall as
+    the K + W pyramids fit in REF_ARM_BUDGET_S — the whole image when they
+    do (configs[3] at K = 5), a declared band otherwise (configs[4]'s 16 GiB
+    image never: more than the reference's ~4 copies fit in host RAM). Rows
+    are a multiple of 2^levels. W untimed pyramids, then the median of K."""
     n, rank, _ = dist_setup()
     if rank != 0:
         return 0
@@ -213,18 +218,21 @@ def run_reference_arm(args, wl):
     from oracle import dwt_oracle as O
     cores = os.cpu_count() or 1
     size = WORKLOADS[wl][0]
-    rows = size if wl == "c3" else 2048
+    unit = 1 << LEVELS
+    # calibration: one pyramid of a 256-row band
+    cal = R.time_pyramid(WAVELET, SCHEME, O.random_image(size, unit, 1), LEVELS, optimized=OPTIMIZED,
+                         workers=cores, repeats=1)
+    per_pyramid = REF_ARM_BUDGET_S / (args.steps + args.warmup + 2)
+    rows = int(per_pyramid / max(cal, 1e-9) * unit) // unit * unit
+    rows = max(unit, min(rows, size if wl == "c3" else 2048))
     img = O.random_image(size, rows, 1)
-    times = []
-    for i in range(args.warmup + args.steps):
-        t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=cores, repeats=1)
-        if i >= args.warmup:
-            times.append(t)
-    t = statistics.median(times)
+    R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=cores, repeats=max(1, args.warmup))
+    t = R.time_pyramid(WAVELET, SCHEME, img, LEVELS, optimized=OPTIMIZED, workers=cores, repeats=args.steps)
     v = size * rows / t / 1e9
     sample = (f"{'full ' if rows == size else ''}{size}x{rows} {'image' if rows == size else 'row band of the image'}"
-              f" (LCG seed 1), 8-level Mallat loop over the reference compile/run API (oracle/_ref, reference "
-              f"sources, -O3), workers={cores}, median of {len(times)} steps after {args.warmup} warm-up")
+              f" (LCG seed 1) per step, sized so the {args.steps} + {args.warmup} pyramids fit ~{REF_ARM_BUDGET_S:.0f} s; "
+              f"8-level Mallat loop over the reference compile/run API (oracle/_ref, reference sources, -O3), "
+              f"workers={cores}, median of {args.steps} steps after {args.warmup} warm-up")
     line = {
         "metric": METRIC, "value": v, "unit": "Gpixel/s", "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
