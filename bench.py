@@ -301,9 +301,42 @@ def run_single(args, plan, img, out, dev):
     torch.cuda.synchronize()
     level_ms = [statistics.mean(e[l].elapsed_ms(e[l + 1]) for e in all_events) for l in range(LEVELS)]
     level_ms[0] = dom_ms
+
+    # what the deep levels cost in the production chain (no events between
+    # levels, which break the PDL overlap): graphs of M pyramids truncated to
+    # 2, 4 and LEVELS levels, min of 5 replays; per-level differences of
+    # single levels are below the replay noise (a few us), groups are not
+    m = 200
+    graphs = {}
+    for L in (2, 4, LEVELS):
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                plan.forward_mallat(img, L, out=out, scratch=scratch, stream=stream.cuda_stream)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(m):
+                plan.forward_mallat(img, L, out=out, scratch=scratch, stream=stream.cuda_stream)
+        graphs[L] = g
+    totals = {L: None for L in graphs}
+    for _ in range(5):  # interleaved replays: slow drifts hit every length alike
+        for L, g in graphs.items():
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+            b.synchronize()
+            t = a.elapsed_time(b) / m
+            totals[L] = t if totals[L] is None else min(totals[L], t)
+    del graphs
+    marginal = {"levels_1_2": totals[2], "levels_3_4": totals[4] - totals[2],
+                f"levels_5_{LEVELS}": totals[LEVELS] - totals[4]}
     fused12 = launches == args.steps * (LEVELS - 1)
     return {"ms_per_step": ms_per_step, "dom_ms": dom_ms, "fused12": fused12,
-            "levels_ms": [round(x, 5) for x in level_ms], "launches": launches, "clk": clk}
+            "levels_ms": [round(x, 5) for x in level_ms],
+            "levels_marginal_ms": {k: round(v, 5) for k, v in marginal.items()},
+            "launches": launches, "clk": clk}
 
 
 def run_sharded(args, plan, shard, img, out, dev, n):
@@ -491,6 +524,12 @@ def main():
             "ns_per_pixel": r["ms_per_step"] * 1e6 / pixels,
             "pyramid_hbm_gbs_per_gpu": pyr_bytes / (r["ms_per_step"] * 1e-3) / 1e9,
             "levels_ms": r["levels_ms"],
+            "levels_ms_note": ("levels_ms: per-level kernel time from events recorded between the levels of an "
+                               "untimed graph (the events serialise the PDL chain, so deep levels show their full "
+                               "launch latency); levels_marginal_ms: what level groups add to the graph-timed "
+                               "pyramid without events (T(4) - T(2), T(8) - T(4); min of 5 replays of 200 "
+                               "pyramids)") if "levels_marginal_ms" in r else None,
+            "levels_marginal_ms": r.get("levels_marginal_ms"),
             "roofline": roofline_entry(achieved, peak, peak_src, dom_bytes, r["dom_ms"], kernel_desc,
                                        ncu_traffic("ncu_pair_summary.json" if r["fused12"] else "ncu_level1_summary.json")
                                        if (wl == "c3" and n == 1) else None),
