@@ -489,3 +489,37 @@ def test_custom_definition_wavelet_on_gpu(dwt, cuda, tmp_path):
         ref, _ = R.run(str(f), s, planes)
         for j in range(4):
             assert np.array_equal(got[j], ref[j]), (s, j)
+
+
+def test_symmetric_pyramid_in_a_cuda_graph(dwt, cuda):
+    """The symmetric levels' crop kernel + fused kernel chain (side-stream
+    fork/join for large levels, PDL with the fused kernel's wait at its end
+    for small ones) captured in a CUDA graph and replayed equals eager calls
+    and the per-step generic executor, also forward + inverse."""
+    import torch
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True, extension="symmetric")
+    inv = dwt.Plan("cdf97", "inverse-lifting", extension="symmetric")
+    for (W, H, L) in [(2048, 1536, 7), (8192, 8192, 3)]:  # 8192^2: level 1 on the side-stream path
+        img = torch.from_numpy(O.random_image(W, H, 17)).to(cuda)
+        ref = plan.forward_mallat(img, L)
+        back_ref = inv.inverse_mallat(ref, L)
+        out = torch.zeros_like(img)
+        back = torch.zeros_like(img)
+        st = torch.cuda.Stream()
+        scr = torch.empty(dwt.workspace_bytes(W, H, L) // 4 + 64, device=cuda)
+        with torch.cuda.stream(st):
+            plan.forward_mallat(img, L, out=out, scratch=scr, stream=st.cuda_stream)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            plan.forward_mallat(img, L, out=out, scratch=scr, stream=st.cuda_stream)
+            inv.inverse_mallat(out, L, image=back, scratch=scr, stream=st.cuda_stream)
+        for _ in range(3):
+            out.zero_()
+            back.zero_()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref) and torch.equal(back, back_ref), (W, H, L)
+        assert float((back - img).abs().max()) <= 5e-5
