@@ -291,7 +291,10 @@ def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, monkeypatch):
     plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True).tune(host_band_rows=int(band_rows))
     # H = 1026 / 1028: the default bands leave a 2-row remainder, which the
     # last band absorbs (a 2-row band would be thinner than its halo)
-    for W, H, L in [(256, 320, 3), (128, 96, 1), (128, 1026, 1), (128, 1028, 2), (64, 4100, 2)]:
+    # and deeper pyramids: exactly 3 levels, more levels, a single band, a
+    # band count that leaves a remainder
+    for W, H, L in [(256, 320, 3), (128, 96, 1), (128, 1026, 1), (128, 1028, 2), (64, 4100, 2), (128, 1024, 3),
+                    (256, 512, 6), (96, 2048, 4), (64, 1312, 5)]:
         img = O.random_image(W, H, 21)
         dev = plan.forward_mallat(torch.from_numpy(img).to(cuda), L).cpu().numpy()
         host = plan.forward_mallat_host(img, L)
