@@ -385,7 +385,8 @@ def run_sharded(args, plan, shard, img, out, dev, n):
         t1.record(stream)
         t1.synchronize()
     dist.barrier()
-    total = torch.tensor([t0.elapsed_time(t1)], device=dev)
+    red_dev = torch.device("cpu") if os.environ.get("DWT2D_BENCH_VIRTUAL") == "1" else dev
+    total = torch.tensor([t0.elapsed_time(t1)], device=red_dev)
     dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
 
@@ -440,8 +441,15 @@ def main():
     json_out = os.fdopen(os.dup(1), "w")
     sys.stdout.flush()
     os.dup2(2, 1)
+    # testing hook: DWT2D_BENCH_VIRTUAL=1 puts every rank on cuda:0 (virtual
+    # ranks sharing one GPU, gloo for the host-side collectives) to exercise
+    # the N > 1 path on a one-GPU box; never set by the driver
+    virtual = os.environ.get("DWT2D_BENCH_VIRTUAL") == "1"
+    if virtual:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if virtual else dev  # where all_reduce operands live
     sharded = n > 1 or args.sharded
     if sharded:
         os.environ.setdefault("NCCL_DEBUG", "WARN")
@@ -450,7 +458,10 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29533")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=dev)
+        if virtual:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     plan = dwt.Plan(WAVELET, SCHEME, optimized=OPTIMIZED)
     size = WORKLOADS[wl][0]
@@ -495,7 +506,7 @@ def main():
         e2e_t.append(time.perf_counter() - a)
     e2e_s = statistics.median(e2e_t)
     if sharded:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert torch.equal(host_out.to(dev), out), "end-to-end entry point disagrees with the device pyramid"
