@@ -99,15 +99,18 @@ struct Meta {
 };
 
 // value of component-column `col` of this lane's row, fetching from the
-// neighbouring lane when col is outside [0, CW)
+// lane that holds it when col is outside [0, CW) (one shuffle, over as many
+// lanes as the column is away)
 template <int col, int CW>
 __device__ __forceinline__ float fetch(const float (&v)[CW]) {
   if constexpr (col >= 0 && col < CW) {
     return v[col];
   } else if constexpr (col >= CW) {
-    return __shfl_down_sync(0xffffffffu, v[col - CW], 1);
+    constexpr int k = col / CW;
+    return __shfl_down_sync(0xffffffffu, v[col - k * CW], k);
   } else {
-    return __shfl_up_sync(0xffffffffu, v[col + CW], 1);
+    constexpr int k = (-col + CW - 1) / CW;
+    return __shfl_up_sync(0xffffffffu, v[col + k * CW], k);
   }
 }
 
@@ -199,7 +202,8 @@ __host__ __device__ constexpr int pair_col(int p, int half) {
 template <class P, int s, int CW>
 struct StepOrder {
   static constexpr int kMaxKeys = 64;
-  static constexpr int kCols = 3 * CW;  // columns -CW .. 2CW-1 (reach <= CW, Meta)
+  static constexpr int kReach = 4;                  // largest column offset of a tap (gen_plans.cpp)
+  static constexpr int kCols = CW + 2 * kReach;      // columns -kReach .. CW + kReach - 1
   struct Data {
     int nkeys = 0, nblocks = 0;
     int kj[kMaxKeys] = {}, kdn[kMaxKeys] = {};
@@ -237,7 +241,7 @@ struct StepOrder {
         if (row.ident) continue;
         for (int t = row.tb; t < row.te; ++t)
           for (int c = 0; c < CW; ++c)
-            if (key(P::taps[t]) == keys[q]) d.cols[q] |= 1ull << (c + P::taps[t].dm + CW);
+            if (key(P::taps[t]) == keys[q]) d.cols[q] |= 1ull << (c + P::taps[t].dm + kReach);
       }
     }
     if (!sorted || n == 0) {  // one block: all keys, rows in table order
@@ -311,25 +315,26 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
   const float2 nz2 = make_float2(nz, nz);
   sfor<0, O::d.nblocks>([&](auto Q_) {
     constexpr int q = decltype(Q_)::value;
-    // the block's source rows, halo columns included: ext[key][c + CW]; for
+    // the block's source rows, halo columns included: ext[key][c + RX]; for
     // the packed form also every operand pair the taps read, built once per
-    // block (ext2[key][m + CW] = columns m and m + pair_col(0, 1)): pairs
+    // block (ext2[key][m + RX] = columns m and m + pair_col(0, 1)): pairs
     // assembled per tap cost a register move each
     constexpr int NK = O::d.nkeys > 0 ? O::d.nkeys : 1;
     constexpr int POFF = pair_col<PV, CW>(0, 1);
+    constexpr int RX = O::kReach;
     float ext[NK][O::kCols];
     float2 ext2[pack ? NK : 1][O::kCols];
     sfor<O::d.kb[q], O::d.ke[q]>([&](auto K_) {
       constexpr int key = decltype(K_)::value;
       constexpr int k = SC::slot(s, u, nhi - dsign * O::d.kdn[key]), j = O::d.kj[key];
       sfor<0, O::kCols>([&](auto C_) {
-        constexpr int c = decltype(C_)::value - CW;
-        if constexpr ((O::d.cols[key] >> (c + CW)) & 1ull) ext[key][c + CW] = fetch<c, CW>(ring[s][k][j]);
+        constexpr int c = decltype(C_)::value - RX;
+        if constexpr ((O::d.cols[key] >> (c + RX)) & 1ull) ext[key][c + RX] = fetch<c, CW>(ring[s][k][j]);
       });
       if constexpr (pack) {
         sfor<0, O::kCols>([&](auto C_) {
-          constexpr int m = decltype(C_)::value - CW;
-          if constexpr (O::pair_needed(key, m, PV)) ext2[key][m + CW] = make_float2(ext[key][m + CW], ext[key][m + POFF + CW]);
+          constexpr int m = decltype(C_)::value - RX;
+          if constexpr (O::pair_needed(key, m, PV)) ext2[key][m + RX] = make_float2(ext[key][m + RX], ext[key][m + POFF + RX]);
         });
       }
     });
@@ -348,7 +353,7 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
             constexpr int c = decltype(C_)::value;
             constexpr int ca = pair_col<PV, CW>(c, 0), cb = pair_col<PV, CW>(c, 1);
             static_assert(cb - ca == POFF, "pair layout");
-            const float2 v = ext2[key][ca + dm + CW];
+            const float2 v = ext2[key][ca + dm + RX];
             const float2 wv = w == 1.0f ? v : __ffma2_rn(make_float2(w, w), v, nz2);
             if constexpr (first)
               acc[r][c] = wv;
@@ -360,7 +365,7 @@ __device__ __forceinline__ void eval_step(float (&ring)[Meta<P>::S + 1][D][4][CW
         } else {
           sfor<0, CW>([&](auto C_) {
             constexpr int c = decltype(C_)::value;
-            const float v = ext[key][c + dm + CW];
+            const float v = ext[key][c + dm + RX];
             if constexpr (!first && P::kFma)
               acc[r][c] = __fmaf_rn(w, v, acc[r][c]);
             else if constexpr (!first)  // reference rounding: product, then sum
@@ -884,8 +889,12 @@ struct LeanRowWriter {
                      : "memory");
       else if constexpr (CW == 4)
         st_vec(q, make_float4(v[j][0], v[j][1], v[j][2], v[j][3]), j != 0);
-      else
+      else if constexpr (CW == 2)
         st_vec(q, make_float2(v[j][0], v[j][1]), j != 0);
+      else if (j != 0)
+        __stcs(q, v[j][0]);
+      else
+        *q = v[j][0];
     });
   }
 };

@@ -40,18 +40,32 @@ struct PairTraits {
 // last row of the chunk (their outputs are never stored, and no stored
 // output reads them): the warp stays convergent, so the level-2 shuffles
 // need no collective re-convergence blocks.
-template <class P, int VF = kPackedFma>
+// Lanes of a warp that store both levels when each lane owns CW1 level-1
+// columns: the halo lanes on either side cover level 1's reach at CW1
+// columns per lane plus level 2's at CW1 / 2.
+template <class P, int CW1>
+__host__ __device__ constexpr int pair_halo_lanes() {
+  return (Meta<P>::HL + CW1 - 1) / CW1 + (Meta<P>::HL + CW1 / 2 - 1) / (CW1 / 2);
+}
+template <class P, int CW1>
+__host__ __device__ constexpr int pair_lanes() {
+  return 32 - 2 * pair_halo_lanes<P, CW1>();
+}
+
+template <class P, int VF = kPackedFma, int CW1 = 4>
 __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, const int chunk) {
   using M = Meta<P>;
   using SC = Sched<P, 1>;
   constexpr int S = M::S, D = SC::D, UNR1 = SC::UNR, UNR = 2 * UNR1;
-  constexpr int CW1 = 4, CW2 = 2, U = M::U, L = M::L;
+  constexpr int CW2 = CW1 / 2, U = M::U, L = M::L;
+  constexpr int HALO = pair_halo_lanes<P, CW1>(), LANES = pair_lanes<P, CW1>();
   static_assert(PairTraits<P>::ok, "pair engine: CW 4 and a reach of at most 2 columns");
+  static_assert(M::HL == M::HR, "pair engine: symmetric horizontal reach");
   const LevelArgs& a1 = t.l1;
   const LevelArgs& a2 = t.l2;
   const int lane = threadIdx.x & 31;
-  const int xc1 = (strip * kPairLanes - 2 + lane) * CW1;  // level-1 component column of this lane
-  const int xc2 = xc1 / 2;                                // exact: xc1 is a multiple of 4
+  const int xc1 = (strip * LANES - HALO + lane) * CW1;  // level-1 component column of this lane
+  const int xc2 = xc1 / 2;                              // exact: xc1 is a multiple of CW1
   const int m0 = t.m_begin + chunk * t.chunk_rows, m1 = min(t.m_end > 0 ? t.m_end : a2.h2, m0 + t.chunk_rows);
   const int n02 = m0 - U;              // first level-2 input row
   const int rows2 = (m1 - m0) + U + L;
@@ -60,7 +74,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
   const int yfirst1 = n01 - L;         // LL_1 row produced at level-1 iteration 0
   const int yfirst2 = n02 - L;         // level-2 output row at level-2 iteration 0
   const int iters = (rows1 + UNR - 1) / UNR * UNR;
-  const bool core = lane >= 2 && lane < 2 + kPairLanes;
+  const bool core = lane >= HALO && lane < HALO + LANES;
 
   float ring1[S + 1][D][4][CW1];
   float ring2[S + 1][D][4][CW2];

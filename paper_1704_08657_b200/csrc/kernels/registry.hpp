@@ -81,6 +81,7 @@ int level_occupancy() {
 
 template <class P>
 cudaError_t launch_pair(const PairArgs& t, cudaStream_t st) {
+  static_assert(pair_lanes<P, 4>() == kPairLanes, "host strip width (kPairLanes) != the pair kernel's");
   const long long warps = (long long)t.nstrips * t.nchunks;
   if (warps <= 0) return cudaSuccess;
   auto k = pair_kernel<P>;

@@ -22,11 +22,11 @@ __global__ void fill(float* p, long long n) {
     p[i] = (float)((i * 2654435761ull) % 1000003ull) * 1e-6f;
 }
 
-template <int VF, int MINB>
+template <int VF, int MINB, int CW1 = 4>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, MINB) k_pair(const __grid_constant__ PairArgs t) {
   const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
   if (wid >= t.nstrips * t.nchunks) return;
-  pair_item<P, VF>(t, wid % t.nstrips, wid / t.nstrips);
+  pair_item<P, VF, CW1>(t, wid % t.nstrips, wid / t.nstrips);
 }
 
 int main(int argc, char** argv) {
@@ -63,10 +63,11 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(ref.data(), mal, n * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(ref_ll.data(), ll2, n / 4, cudaMemcpyDeviceToHost));
 
-  auto run = [&](const char* name, auto kern, int chunk_override) {
+  auto run = [&](const char* name, auto kern, int chunk_override, int cw1 = 4) {
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, kern));
-    const int smem = staged_bytes<4>();
+    const int smem = cw1 == 4 ? staged_bytes<4>() : staged_bytes<2>();
+    const int lanes = cw1 == 4 ? pair_lanes<P, 4>() : pair_lanes<P, 2>();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarpsPerCta * 32, smem));
@@ -75,7 +76,7 @@ int main(int argc, char** argv) {
     t.l2 = level_args(nullptr, 0, W / 4, H / 4, ll2, W / 4);
     t.l1.staged = 1;
     t.l1.neg_zero = -0.0f;
-    t.nstrips = (t.l1.w2 + kPairLanes * 4 - 1) / (kPairLanes * 4);
+    t.nstrips = (t.l1.w2 + lanes * cw1 - 1) / (lanes * cw1);
     const long long resident = (long long)occ * kWarpsPerCta * sms;
     const long long per_wave = std::max<long long>(1, resident / t.nstrips);
     const int span = t.l2.h2;
@@ -114,7 +115,10 @@ int main(int argc, char** argv) {
     run("VF0 scalar", k_pair<0, 1>, 0);
     run("VF1 (c,c+1)", k_pair<1, 1>, 0);
     run("VF2 (c,c+2)", k_pair<2, 1>, 0);
-    run("VF1 minb3", k_pair<1, 3>, 0);
+    run("CW2 VF1", k_pair<1, 1, 2>, 0, 2);
+    run("CW2 VF1 minb4", k_pair<1, 4, 2>, 0, 2);
+    run("CW2 VF0 minb4", k_pair<0, 4, 2>, 0, 2);
+    run("CW2 VF1 ch128", k_pair<1, 4, 2>, 128, 2);
   }
   return 0;
 }
