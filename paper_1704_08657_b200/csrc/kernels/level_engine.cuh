@@ -123,7 +123,17 @@ __device__ __forceinline__ float fetch(const float (&v)[CW]) {
 // indexed by (row mod slots); the main loop is unrolled by UNR = lcm of all
 // slot counts so every slot index is a compile-time constant and rows never
 // move between registers. If that lcm is large (wide convolution windows),
-// the windows shift instead (register moves, UNR = slots of window 0).
+// windows 1..S shift instead (register moves, UNR = slots of window 0).
+// Programs with the kShift trait (the very wide composed convolutions) shift
+// every window, the load ring too, and run the loop body once per row: their
+// 8-fold unrolled body (~80 KB of SASS) does not stay in the instruction
+// cache, and one register move per window value and row costs less.
+template <class P>
+constexpr bool shift_rows() {
+  if constexpr (requires { P::kShift; }) return P::kShift;
+  else return false;
+}
+
 template <class P, int PF>
 struct Sched {
   using M = Meta<P>;
@@ -135,8 +145,13 @@ struct Sched {
     for (int b = 0; b <= S; ++b) l = l / gcd(l, slots(b)) * slots(b);
     return l;
   }
-  static constexpr bool kCirc = lcm_all() <= 8;
-  static constexpr int UNR = kCirc ? lcm_all() : slots(0);
+  static constexpr bool kShift0 = shift_rows<P>();
+  static constexpr int shift_unroll() {
+    if constexpr (requires { P::kShiftUnroll; }) return P::kShiftUnroll;
+    else return 1;
+  }
+  static constexpr bool kCirc = !kShift0 && lcm_all() <= 8;
+  static constexpr int UNR = kShift0 ? shift_unroll() : kCirc ? lcm_all() : slots(0);
   static constexpr int DMAX() {
     int v = 1;
     for (int b = 0; b <= S; ++b) v = cmax(v, slots(b));
@@ -144,10 +159,12 @@ struct Sched {
   }
   static constexpr int D = DMAX();
   // register slot of the row `age` rows older than the newest row of window
-  // b, at unrolled iteration u (circular mode); age itself in shift mode
-  // (window 0 is always circular: it is the load ring)
+  // b, at unrolled iteration u (circular mode); age itself in shift mode.
+  // Window 0 is the load ring: circular unless kShift0, where row i (age 0)
+  // sits in slot PF - 1 and the rows in flight (ages -1 .. -PF + 1) below it.
   static constexpr int slot(int b, int u, int age) {
     const int n = slots(b);
+    if (b == 0 && kShift0) return age + PF - 1;
     return (kCirc || b == 0) ? ((u - age) % n + n) % n : age;
   }
 };
@@ -924,7 +941,7 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   const int ys0 = max(y0, a.keep_y0), ys1 = min(y1, a.keep_y1 > 0 ? a.keep_y1 : a.h2);  // rows stored
 
   float ring[S + 1][D][4][CW];
-  sfor<1, S + 1>([&](auto B_) {
+  sfor<SC::kShift0 ? 0 : 1, S + 1>([&](auto B_) {
     sfor<0, D>([&](auto K_) {
       sfor<0, 4>([&](auto J_) {
         sfor<0, CW>([&](auto C_) {
@@ -942,7 +959,7 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   // prologue: rows n0 .. n0+PF-1 land in the slots iteration 0.. expect
   sfor<0, PF>([&](auto U_) {
     constexpr int u = decltype(U_)::value;
-    rd.load(a, ring[0][SC::slot(0, u, 0)]);
+    rd.load(a, ring[0][SC::slot(0, 0, -u)]);
   });
 
   for (int it = 0; it < iters; it += UNR) {
@@ -965,8 +982,21 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
         });
       }
       eval_step<P, PF, 0, u, D, CW, UPW, VF>(ring, a.neg_zero);
-      // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row i + PF
-      if (i + PF < rows) rd.load(a, ring[0][SC::slot(0, u, -PF)]);
+      // window 0 no longer needs row i - depth(0) + 1: reuse its slot for row
+      // i + PF (kShift0: move every row one slot up, the new one into slot 0)
+      if constexpr (SC::kShift0) {
+        sfor<1, NS0>([&](auto K_) {
+          constexpr int k = NS0 - decltype(K_)::value;  // NS0-1 .. 1
+          sfor<0, 4>([&](auto J_) {
+            sfor<0, CW>([&](auto C_) {
+              ring[0][k][decltype(J_)::value][decltype(C_)::value] = ring[0][k - 1][decltype(J_)::value][decltype(C_)::value];
+            });
+          });
+        });
+        if (i + PF < rows) rd.load(a, ring[0][0]);
+      } else if (i + PF < rows) {
+        rd.load(a, ring[0][SC::slot(0, u, -PF)]);
+      }
       sfor<1, S>([&](auto S_) { eval_step<P, PF, decltype(S_)::value, u, D, CW, UPW, VF>(ring, a.neg_zero); });
       const int y = UPW ? yfirst - i : yfirst + i;
       if (y >= ys0 && y < ys1 && out_lane) wr.store(ring[S][SC::slot(S, u, 0)]);

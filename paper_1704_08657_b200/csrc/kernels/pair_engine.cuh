@@ -32,7 +32,7 @@ namespace gpu {
 template <class P>
 struct PairTraits {
   using M = Meta<P>;
-  static constexpr bool ok = P::kCW == 4 && M::HL <= 2 && M::HR <= 2;
+  static constexpr bool ok = P::kCW == 4 && M::HL <= 2 && M::HR <= 2 && !shift_rows<P>();
 };
 
 // VF: packed-FMA form of the sub-steps (level_engine.cuh: eval_step).
@@ -56,6 +56,7 @@ template <class P, int VF = kPackedFma, int CW1 = 4>
 __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, const int chunk) {
   using M = Meta<P>;
   using SC = Sched<P, 1>;
+  static_assert(!SC::kShift0, "level pair: circular load ring");
   constexpr int S = M::S, D = SC::D, UNR1 = SC::UNR, UNR = 2 * UNR1;
   constexpr int CW2 = CW1 / 2, U = M::U, L = M::L;
   constexpr int HALO = pair_halo_lanes<P, CW1>(), LANES = pair_lanes<P, CW1>();

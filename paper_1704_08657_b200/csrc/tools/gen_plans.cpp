@@ -41,6 +41,7 @@ struct Gen {
   StepProgram prog;
   int cw;
   bool pack;  // composed programs: packed FP32 arithmetic
+  bool shift = false;  // shifted register windows, one loop body per row
 };
 
 }  // namespace
@@ -81,9 +82,21 @@ int main(int argc, char** argv) {
       // 445 vs 501 us, polyconvolution 710 vs 742 us, and spill-free unlike
       // CW=4 at 901 us); CW=4 composed programs are packed (non-separable
       // lifting 430 vs 481 us). scripts/tune_composed.cu.
+      //
+      // The widest programs (>= 128 taps per quad: CDF 9/7 non-separable
+      // convolution and polyconvolution baseline, non-separable convolution
+      // optimized) shift their register windows (kShift, level_engine.cuh:
+      // Sched) and run one loop body per row at CW=4, scalar: the unrolled
+      // body did not stay in the instruction cache. 16384^2 / 4096^2:
+      // non-separable convolution baseline 1264 / 98.6 us (was 1775 / 150.5
+      // packed at CW=2), polyconvolution baseline 644 / 50.9 (719 / 77.9),
+      // non-separable convolution optimized 506 / 43.9 (537 / 45.6); the
+      // 64-tap CDF 5/3 ones and the separable convolutions measured no gain
+      // or a loss (scripts/tune_composed.cu, SHIFT_ONLY=1).
       const bool fma = g.prog.fused_multiply_add;
-      g.cw = (reach <= 2 && (fma ? depth >= 4 : (depth >= 4 || step_taps >= 64))) ? 2 : 4;
-      g.pack = fma || g.cw == 4 || step_taps > 128;
+      g.shift = reach <= 2 && g.prog.taps_per_quad() >= 128;
+      g.cw = !g.shift && (reach <= 2 && (fma ? depth >= 4 : (depth >= 4 || step_taps >= 64))) ? 2 : 4;
+      g.pack = g.shift ? fma : (fma || g.cw == 4 || step_taps > 128);
       if (reach > 4) {
         std::cerr << "plan " << g.name << " reaches " << reach << " columns; unsupported\n";
         std::exit(1);
@@ -140,6 +153,7 @@ int main(int argc, char** argv) {
     h << "  static constexpr int kCW = " << g.cw << ";\n";
     h << "  static constexpr bool kFma = " << (p.fused_multiply_add ? "true" : "false") << ";\n";
     h << "  static constexpr bool kPack = " << (g.pack ? "true" : "false") << ";\n";
+    if (g.shift) h << "  static constexpr bool kShift = true;\n";
     // bottom-up odd chunks (level_engine.cuh: level_dispatch) for programs
     // with short sub-steps; the wide composed steps (non-separable
     // convolution / polyconvolution / lifting baselines) lose more to the
