@@ -940,8 +940,12 @@ __device__ __forceinline__ void level_item(const LevelArgs& a, const int wid, co
   bool out_lane = lane >= 1 && lane <= kOutLanes;
   const int ys0 = max(y0, a.keep_y0), ys1 = min(y1, a.keep_y1 > 0 ? a.keep_y1 : a.h2);  // rows stored
 
+  // every window starts zeroed, the load ring too: warm-up iterations read
+  // slots no row has been loaded into yet (their outputs are discarded), and
+  // values the compiler may treat as undefined there have been seen to change
+  // stored outputs (the shifted-window schedule)
   float ring[S + 1][D][4][CW];
-  sfor<SC::kShift0 ? 0 : 1, S + 1>([&](auto B_) {
+  sfor<0, S + 1>([&](auto B_) {
     sfor<0, D>([&](auto K_) {
       sfor<0, 4>([&](auto J_) {
         sfor<0, CW>([&](auto C_) {

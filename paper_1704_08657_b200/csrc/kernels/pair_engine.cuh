@@ -80,7 +80,7 @@ __device__ __forceinline__ void pair_item(const PairArgs& t, const int strip, co
   float ring1[S + 1][D][4][CW1];
   float ring2[S + 1][D][4][CW2];
   float pend[2][CW2];  // (ee, oe) of the last even LL_1 row
-  sfor<1, S + 1>([&](auto B_) {
+  sfor<0, S + 1>([&](auto B_) {  // all windows zeroed (level_engine.cuh: level_item)
     sfor<0, D>([&](auto K_) {
       sfor<0, 4>([&](auto J_) {
         constexpr int b = decltype(B_)::value, k = decltype(K_)::value, j = decltype(J_)::value;
