@@ -149,7 +149,7 @@ cudaError_t preload_entry() {
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, true>));
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, false>));
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, true, false, true, true>));
-    if constexpr (PairTraits<P>::ok && P::kAlt) load(reinterpret_cast<const void*>(pair_kernel<P>));
+    if constexpr (PairTraits<P>::ok && (P::kAlt || P::kFma)) load(reinterpret_cast<const void*>(pair_kernel<P>));
   } else {
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, true, true>));
     load(reinterpret_cast<const void*>(level_kernel<P, kPrefetchRows, false, true, false>));
@@ -178,7 +178,7 @@ PlanEntry make_entry() {
   if constexpr (kForward) {
     e.from_image = &launch_level<P, true, false>;
     e.occupancy = &level_occupancy<P, true, false>;
-    if constexpr (PairTraits<P>::ok && P::kAlt) {
+    if constexpr (PairTraits<P>::ok && (P::kAlt || P::kFma)) {
       e.pair = &launch_pair<P>;
       e.pair_occupancy = &pair_occupancy<P>;
     }

@@ -42,6 +42,7 @@ struct Gen {
   int cw;
   bool pack;  // composed programs: packed FP32 arithmetic
   bool shift = false;  // shifted register windows, one loop body per row
+  int depth = 1;       // deepest row window of a sub-step
 };
 
 }  // namespace
@@ -69,6 +70,7 @@ int main(int argc, char** argv) {
       // registers when their horizontal reach allows it
       int depth = 1;
       for (const KernelStep& st : g.prog.steps) depth = std::max(depth, st.max_dn - st.min_dn + 1);
+      g.depth = depth;
       std::size_t step_taps = 0;
       for (const KernelStep& st : g.prog.steps) {
         std::size_t n = 0;
@@ -95,7 +97,9 @@ int main(int argc, char** argv) {
       // or a loss (scripts/tune_composed.cu, SHIFT_ONLY=1).
       const bool fma = g.prog.fused_multiply_add;
       g.shift = reach <= 2 && g.prog.taps_per_quad() >= 128;
-      g.cw = !g.shift && (reach <= 2 && (fma ? depth >= 4 : (depth >= 4 || step_taps >= 64))) ? 2 : 4;
+      // Factored (FMA) programs all take CW=4 (with TMA staging at 16384^2
+      // the separable convolution optimized runs 362 vs 422 us at CW=2).
+      g.cw = !fma && !g.shift && reach <= 2 && (depth >= 4 || step_taps >= 64) ? 2 : 4;
       g.pack = g.shift ? fma : (fma || g.cw == 4 || step_taps > 128);
       if (reach > 4) {
         std::cerr << "plan " << g.name << " reaches " << reach << " columns; unsupported\n";
@@ -160,7 +164,11 @@ int main(int argc, char** argv) {
     // second unrolled body's register pressure than the L2 reuse gains
     // (measured at 4096^2: e.g. non-separable convolution baseline 0.22 vs
     // 0.48 ms, optimized non-separable lifting 32.8 vs 30.7 us)
-    const bool alt = p.fused_multiply_add || p.taps_per_quad() <= 8 * (long)p.steps.size();
+    // Round 2, TMA-staged 16384^2 levels: the convolution-shaped factored
+    // programs (row windows of 3 or more) lose with it too (separable
+    // convolution optimized 462 vs 378 us, polyconvolution optimized 386 vs
+    // 357; the lifting ones gain: 342 vs 360), scripts/probe_pair_programs.py
+    const bool alt = g.depth <= 2 && (p.fused_multiply_add || p.taps_per_quad() <= 8 * (long)p.steps.size());
     h << "  static constexpr bool kAlt = " << (alt ? "true" : "false") << ";\n";
     h << "  static constexpr int kTaps = " << std::max<std::size_t>(taps.size(), 1) << ";\n";
     h << "  static constexpr RowDesc rows[" << rows.size() << "] = {";

@@ -35,9 +35,16 @@ struct VU : B {
   static constexpr int kShiftUnroll = U;
 };
 
-template <class P, int PF = 2, bool STAGED = false>
+// factored programs: packed-FMA form VF of the level kernel's sub-steps
+template <class P, int VF>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_level_vf(const LevelArgs a) {
+  const int wid = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+  if (wid < a.nstrips * a.nchunks) level_item<P, 2, true, false, true, false, false, void, VF>(a, wid, wid / a.nstrips);
+}
+
+template <class P, int PF = 2, bool STAGED = false, int VF = -1>
 void run(const char* name, int W, float* img, float* out, std::vector<float>& ref, bool first) {
-  auto kern = level_kernel<P, STAGED ? 1 : PF, true, false, true, STAGED>;
+  auto kern = VF >= 0 ? k_level_vf<P, VF < 0 ? 0 : VF> : level_kernel<P, STAGED ? 1 : PF, true, false, true, STAGED>;
   const int smem = STAGED ? staged_bytes<P::kCW>() : 0;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaFuncAttributes fa;
@@ -111,6 +118,40 @@ int main() {
     CK(cudaMalloc(&out, n * 4));
     fill<<<1184, 256>>>(img, (long long)n);
     std::vector<float> ref;
+    if (getenv("TMA_ONLY")) {
+      run<V<cdf97_nonseparable_convolution_opt, 4, true, true>>("nsconv-opt CW4 shift", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_convolution_opt, 4, true, true>, 1, true>("nsconv-opt CW4 shift TMA", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_convolution_opt, 4, true>, 1, true>("nsconv-opt CW4 TMA", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_opt, 2, true>>("sepconv-opt CW2", W, img, out, ref, true);
+      run<V<cdf97_separable_convolution_opt, 4, true>, 1, true>("sepconv-opt CW4 TMA", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_opt, 4, true, true>, 1, true>("sepconv-opt CW4 shift TMA", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_base, 2, false>>("sepconv CW2 scalar", W, img, out, ref, true);
+      run<V<cdf97_separable_convolution_base, 4, true>, 1, true>("sepconv CW4 packed TMA", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_base, 4, false>, 1, true>("sepconv CW4 scalar TMA", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_base, 4, true, true>, 1, true>("sepconv CW4 packed shift TMA", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_polyconvolution_base, 4, false, true>>("polyconv CW4 scalar shift", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_polyconvolution_base, 4, true, true>, 1, true>("polyconv CW4 packed shift TMA", W, img, out, ref, false);
+      cudaFree(img), cudaFree(out);
+      continue;
+    }
+    if (getenv("VF_ONLY")) {
+      run<V<cdf97_nonseparable_convolution_opt, 4, true, true>>("nsconv-opt CW4 shift", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_convolution_opt, 4, true, true>, 2, false, 1>("nsconv-opt CW4 shift VF1", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_convolution_opt, 4, true, true>, 2, false, 2>("nsconv-opt CW4 shift VF2", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_convolution_opt, 2, true, true>, 2, false, 1>("nsconv-opt CW2 shift VF1", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_opt, 2, true>>("sepconv-opt CW2", W, img, out, ref, true);
+      run<V<cdf97_separable_convolution_opt, 2, true>, 2, false, 1>("sepconv-opt CW2 VF1", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_opt, 4, true>, 2, false, 1>("sepconv-opt CW4 VF1", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_opt, 4, true>, 2, false, 2>("sepconv-opt CW4 VF2", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_polyconvolution_opt, 4, true>>("polyconv-opt CW4", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_polyconvolution_opt, 4, true>, 2, false, 1>("polyconv-opt CW4 VF1", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_polyconvolution_opt, 4, true>, 2, false, 2>("polyconv-opt CW4 VF2", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_base, 2, false>>("sepconv CW2 scalar", W, img, out, ref, true);
+      run<V<cdf97_separable_convolution_base, 4, true>>("sepconv CW4 packed", W, img, out, ref, false);
+      run<V<cdf97_separable_convolution_base, 4, true>, 1>("sepconv CW4 packed PF1", W, img, out, ref, false);
+      cudaFree(img), cudaFree(out);
+      continue;
+    }
     if (getenv("SHIFT_ONLY")) {
       run<V<cdf97_nonseparable_convolution_base, 2, true>>("nsconv CW2 packed", W, img, out, ref, true);
       run<V<cdf97_nonseparable_convolution_base, 2, false, true>>("nsconv CW2 scalar shift", W, img, out, ref, false);

@@ -237,7 +237,8 @@ def test_tma_staged_inverse_levels_bit_exact(dwt, cuda, w, monkeypatch):
 
 @pytest.mark.parametrize("w,s,opt", [("cdf97", "nonseparable-lifting", True), ("cdf53", "separable-lifting", False),
                                      ("cdf97", "separable-lifting", True),
-                                     ("cdf97", "nonseparable-polyconvolution", True)])
+                                     ("cdf97", "nonseparable-polyconvolution", True),
+                                     ("cdf97", "separable-convolution", True)])
 def test_level_pair_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
     """Levels 1 + 2 in one pass (LL_1 kept in registers, pair_engine.cuh;
     forced on every size with DWT2D_PAIR=2) give the same bits as one launch
