@@ -118,6 +118,16 @@ int main() {
     CK(cudaMalloc(&out, n * 4));
     fill<<<1184, 256>>>(img, (long long)n);
     std::vector<float> ref;
+    if (getenv("PACK_ONLY")) {
+      run<V<cdf97_nonseparable_convolution_base, 4, false, true>>("nsconv CW4 scalar shift", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_convolution_base, 4, true, true>, 1>("nsconv CW4 packed shift PF1", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_convolution_base, 4, true, true>, 1, true>("nsconv CW4 packed shift TMA", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_convolution_base, 2, true, true>, 1, true>("nsconv CW2 packed shift TMA", W, img, out, ref, false);
+      run<V<cdf97_nonseparable_polyconvolution_base, 4, false, true>>("polyconv CW4 scalar shift", W, img, out, ref, true);
+      run<V<cdf97_nonseparable_polyconvolution_base, 4, true, true>, 1>("polyconv CW4 packed shift PF1", W, img, out, ref, false);
+      cudaFree(img), cudaFree(out);
+      continue;
+    }
     if (getenv("TMA_ONLY")) {
       run<V<cdf97_nonseparable_convolution_opt, 4, true, true>>("nsconv-opt CW4 shift", W, img, out, ref, true);
       run<V<cdf97_nonseparable_convolution_opt, 4, true, true>, 1, true>("nsconv-opt CW4 shift TMA", W, img, out, ref, false);
