@@ -339,10 +339,8 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_stream() {
-  static thread_local SideStream per_dev[16];
-  int dev = 0;
-  cuda_check(cudaGetDevice(&dev), "device");
-  SideStream& ss = per_dev[dev & 15];
+  static thread_local SideStream per_dev[kMaxDevices];
+  SideStream& ss = per_dev[current_device()];
   if (!ss.s) {
     cuda_check(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking), "side stream");
     cuda_check(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming), "fork event");
