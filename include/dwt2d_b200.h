@@ -131,7 +131,9 @@ DWT2D_B200_API void dwt2d_plan_destroy(dwt2d_plan* plan);
  * variables when the plan is created; never read on the launch path.
  * Names: "pdl" (0/1), "chunk_rows" (0 = policy), "alternate" (0/1/2), "tma"
  * (0 off, 1 policy, 2 forced), "pair" (0 off, 1 policy, 2 forced),
- * "pair_chunk_rows", "crop_tiles" (0/1), "crop_core", "host_band_rows".
+ * "pair_chunk_rows", "crop_tiles" (0/1), "crop_core", "host_band_rows",
+ * "host_levels" (levels pipelined by row bands in the host entry point,
+ * 0 = policy, at most 3).
  * Unknown names: DWT2D_EINVAL. Not thread-safe against concurrent launches
  * with the same plan. */
 DWT2D_B200_API int dwt2d_plan_set_tuning(dwt2d_plan* plan, const char* name, int value);

@@ -39,6 +39,7 @@ struct Tuning {
                             // with the fused kernel, 1 one generic tile launch after it, 0 per sub-step
   int crop_core = 12;       // DWT2D_CROP_CORE: positions per crop tile (capped by the crop kernel's 256 cells)
   int host_band_rows = 0;   // DWT2D_HOST_BAND_ROWS: image rows per host pipeline band (0: policy)
+  int host_levels = 0;      // DWT2D_HOST_LEVELS: levels pipelined by bands in the host entry point (0: policy)
 };
 
 namespace {
@@ -57,6 +58,7 @@ Tuning tuning_from_env() {
   t.crop_tiles = env_int("DWT2D_CROP_TILES", t.crop_tiles);
   t.crop_core = std::max(1, env_int("DWT2D_CROP_CORE", t.crop_core));
   t.host_band_rows = env_int("DWT2D_HOST_BAND_ROWS", t.host_band_rows);
+  t.host_levels = env_int("DWT2D_HOST_LEVELS", t.host_levels);
   return t;
 }
 }  // namespace
@@ -1449,31 +1451,85 @@ void band_details_down(float* hdet, const float* det, int W, int w_in, int h_in,
              "D2H");
 }
 
+// Host image -> pyramid -> host with the copies overlapped (SURVEY §8(d)
+// e2e). The image goes up in row bands on the `up` stream; the first P
+// levels run band by band on `comp` and each band's detail rows go down on
+// `down` while later bands upload.
+//
+// Compute bands trail the upload bands by the bottom halo: level l's band b
+// covers input rows [C_l(b), C_l(b+1)) with C_l(b) = floor4(E_l(b) - 2*down),
+// where E_1(b) is the upload boundary and E_l(b) = C_{l-1}(b) / 2 the LL rows
+// level l-1 has produced; so band b of every level runs as soon as image band
+// b has landed (its bottom halo is already there) instead of waiting for band
+// b + 1. Band 0's periodic top halo at level l is the TAIL of level l's input
+// (its last 2*up rows): the image's last T_1 rows go up first, and the LL
+// tails are computed early from them (T_l = 2 T_{l+1} + 2 up input rows of
+// level l, T_P = 2 up); the last band recomputes those rows with identical
+// values. Levels P+1.. run on the device-resident LL_P, and only its
+// quadrant goes down last.
 void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int W, int H, int levels,
                                    float* out) {
   HostPipe& hp = host_pipe();
   const int U = p.up, Ld = p.down;
-  const size_t n = size_t(W) * H, q = size_t(W / 2) * (H / 2), q2 = q / 4;
-  const int w2 = W / 2, h2 = H / 2, w4 = W / 4, h4 = H / 4;
-  const bool two = levels >= 2;  // level 2 is pipelined by bands as well
-  const int tail_rows = two ? 6 * U : 2 * U;  // uploaded first (periodic halos of band 0)
-  if (tail_rows + 2 * Ld > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
-  const size_t sub_ws = levels > 2 ? dwt2d_workspace_bytes(w4, h4, levels - 2) : 0;
-  const size_t bytes = (2 * n + q + q2) * 4 + sub_ws + 512;
-  float* d_img = static_cast<float*>(hp.reserve(bytes));
+  const Bands bands = bands_for(p, H, std::max(U, Ld) * 2);
+  const int B = bands.n;
+  // pipelined levels: 2 by default (16384^2 e2e, 8 levels: 24.2 ms with 2,
+  // 24.9 ms with 3 — level-3 bands of a few MB cost more in launches and
+  // small copies than the 48 MiB they take off the last copy — and 27.5 ms
+  // with 1), at most 3; fewer when the bands would get thinner than 4 halos
+  // or the tails would not fit in the level inputs
+  constexpr int kMaxPipe = 3;
+  int P = std::min(levels, p.tune.host_levels > 0 ? std::min(p.tune.host_levels, kMaxPipe) : 2);
+  std::vector<std::vector<int>> C;  // C[l - 1][b], b = 0..B
+  std::vector<int> T;               // T[l - 1]: tail rows of level l's input uploaded/computed early
+  for (;; --P) {
+    C.assign(P, std::vector<int>(B + 1));
+    T.assign(P + 1, 0);
+    bool ok = true;
+    T[P - 1] = 2 * U;
+    for (int l = P - 1; l >= 1; --l) T[l - 1] = 2 * T[l] + 2 * U;
+    for (int l = 1; l <= P && ok; ++l) {
+      const int hl = H >> (l - 1);
+      C[l - 1][0] = 0, C[l - 1][B] = hl;
+      for (int b = 1; b < B; ++b) {
+        const int e = l == 1 ? bands.begin(b) : C[l - 2][b] / 2;
+        C[l - 1][b] = ((e - 2 * Ld) / 4) * 4;
+      }
+      for (int b = 0; b < B; ++b) ok = ok && C[l - 1][b + 1] - C[l - 1][b] >= 4 * std::max(U, Ld);
+      if (l < P) ok = ok && hl - 2 * T[l] >= 2 * U + 2 * Ld && hl - 2 * T[l] >= C[l - 1][std::min(1, B)];
+    }
+    ok = ok && T[0] + 2 * Ld <= H;
+    if (ok || P == 1) break;
+  }
+  if (T[0] + 2 * Ld > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
+
+  // device buffers: image, Mallat output, LL_1 .. LL_P (LL_levels goes into
+  // the output), workspace of the device-resident levels
+  const size_t n = size_t(W) * H;
+  std::vector<size_t> ll_off(P + 1, 0);
+  size_t floats = 2 * n;
+  for (int l = 1; l <= P; ++l) {
+    ll_off[l] = floats;
+    floats += ((size_t(W >> l) * size_t(H >> l)) + 63) & ~size_t(63);
+  }
+  const int wP = W >> P, hP = H >> P;
+  const size_t sub_ws = levels > P ? dwt2d_workspace_bytes(wP, hP, levels - P) : 0;
+  float* d_img = static_cast<float*>(hp.reserve(floats * 4 + sub_ws + 512));
   float* d_out = d_img + n;
-  float* d_ll1 = d_out + n;
-  float* d_ll2 = d_ll1 + ((q + 63) & ~size_t(63));
-  float* d_sub = d_ll2 + ((q2 + 63) & ~size_t(63));
+  float* d_sub = d_img + floats;
+  auto ll = [&](int l) { return l == levels ? d_out : d_img + ll_off[l]; };
+  auto llp = [&](int l) { return l == levels ? size_t(W) : size_t(W >> l); };
+  auto in_of = [&](int l) { return l == 1 ? d_img : ll(l - 1); };
+  auto inp_of = [&](int l) { return l == 1 ? size_t(W) : llp(l - 1); };
+
   size_t ev = 0;
   cudaEvent_t ev_alloc = hp.event(ev++);
   cuda_check(cudaEventRecord(ev_alloc, hp.comp), "record");
   cuda_check(cudaStreamWaitEvent(hp.up, ev_alloc), "wait");
   cuda_check(cudaStreamWaitEvent(hp.down, ev_alloc), "wait");
 
-  const Bands bands = bands_for(p, H, std::max(U, Ld) * 2);
-  const int B = bands.n;
-  // upload: the image's last rows first, then the bands in order
+  // upload: the image's last T_1 rows first, then the bands in order
+  const int tail_rows = T[0];
   const size_t tail0 = size_t(H - tail_rows) * W;
   cuda_check(cudaMemcpyAsync(d_img + tail0, image + tail0, size_t(tail_rows) * W * 4, cudaMemcpyHostToDevice, hp.up),
              "H2D");
@@ -1488,10 +1544,6 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     up[b] = hp.event(ev++);
     cuda_check(cudaEventRecord(up[b], hp.up), "record");
   }
-  float* ll1 = two ? d_ll1 : d_out;  // a one-level pyramid writes LL straight into place
-  const size_t ll1p = two ? size_t(w2) : size_t(W);
-  float* ll2 = levels == 2 ? d_out : d_ll2;
-  const size_t ll2p = levels == 2 ? size_t(W) : size_t(w4);
 
   auto down_after = [&](auto&& copy) {
     cudaEvent_t done = hp.event(ev++);
@@ -1499,28 +1551,25 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     cuda_check(cudaStreamWaitEvent(hp.down, done), "wait");
     copy();
   };
-  auto level2_band = [&](int b) {
-    const int r0 = bands.begin(b) / 2, r1 = bands.end(b, H) / 2;  // LL1 rows of band b
-    band_level(p, d_ll1, size_t(w2), w2, h2, r0, r1, ll2, ll2p, d_out, size_t(W), hp.comp);
-    down_after([&] { band_details_down(out, d_out, W, w2, h2, r0 / 2, (r1 - r0) / 2, hp.down); });
+  auto level_band = [&](int l, int b) {
+    const int wl = W >> (l - 1), hl = H >> (l - 1), r0 = C[l - 1][b], r1 = C[l - 1][b + 1];
+    band_level(p, in_of(l), inp_of(l), wl, hl, r0, r1, ll(l), llp(l), d_out, size_t(W), hp.comp);
+    down_after([&] { band_details_down(out, d_out, W, wl, hl, r0 / 2, (r1 - r0) / 2, hp.down); });
   };
 
-  if (two) {  // LL1's last 2U rows early: band 0's periodic top halo at level 2
-    cuda_check(cudaStreamWaitEvent(hp.comp, up[0]), "wait");
-    band_level(p, d_img, size_t(W), W, H, H - 4 * U, H, ll1, ll1p, d_out, size_t(W), hp.comp);
-  }
   for (int b = 0; b < B; ++b) {
-    const int r0 = bands.begin(b), r1 = bands.end(b, H);
-    cuda_check(cudaStreamWaitEvent(hp.comp, up[std::min(b + 1, B - 1)]), "wait");  // bottom halo = band b + 1
-    band_level(p, d_img, size_t(W), W, H, r0, r1, ll1, ll1p, d_out, size_t(W), hp.comp);
-    down_after([&] { band_details_down(out, d_out, W, W, H, r0 / 2, (r1 - r0) / 2, hp.down); });
-    if (two && b >= 1) level2_band(b - 1);  // its bottom halo (LL1 of band b) is ready now
+    cuda_check(cudaStreamWaitEvent(hp.comp, up[b]), "wait");
+    for (int l = 1; l <= P; ++l) {
+      level_band(l, b);
+      if (b == 0 && l < P) {  // LL_l's tail: band 0's top halo at level l + 1 (and the next tail's input)
+        const int wl = W >> (l - 1), hl = H >> (l - 1);
+        band_level(p, in_of(l), inp_of(l), wl, hl, hl - 2 * T[l], hl, ll(l), llp(l), d_out, size_t(W), hp.comp);
+      }
+    }
   }
-  if (two) level2_band(B - 1);
-  if (levels > 2) forward_mallat(p, d_ll2, size_t(w4), w4, h4, levels - 2, d_out, size_t(W), d_sub, hp.comp);
-  const int wq = two ? w4 : w2, hq = two ? h4 : h2;  // the remaining top-left corner
-  down_after([&] {
-    cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(wq) * 4, hq,
+  if (levels > P) forward_mallat(p, ll(P), llp(P), wP, hP, levels - P, d_out, size_t(W), d_sub, hp.comp);
+  down_after([&] {  // the remaining top-left corner (levels > P and LL_levels)
+    cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(wP) * 4, hP,
                                  cudaMemcpyDeviceToHost, hp.down),
                "D2H");
   });
@@ -1605,6 +1654,7 @@ int dwt2d_plan_set_tuning(dwt2d_plan* p, const char* name, int value) {
     else if (n == "crop_tiles") t.crop_tiles = value;
     else if (n == "crop_core") t.crop_core = std::max(1, value);
     else if (n == "host_band_rows") t.host_band_rows = value;
+    else if (n == "host_levels") t.host_levels = value;
     else fail(DWT2D_EINVAL, "unknown tuning switch: " + n);
   });
 }
