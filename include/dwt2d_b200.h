@@ -133,7 +133,7 @@ DWT2D_B200_API void dwt2d_plan_destroy(dwt2d_plan* plan);
  * (0 off, 1 policy, 2 forced), "pair" (0 off, 1 policy, 2 forced),
  * "pair_chunk_rows", "crop_tiles" (0/1), "crop_core", "host_band_rows",
  * "host_levels" (levels pipelined by row bands in the host entry point,
- * 0 = policy, at most 3).
+ * 0 = policy, at most 3), "host_taper" (0/1: short first and last bands).
  * Unknown names: DWT2D_EINVAL. Not thread-safe against concurrent launches
  * with the same plan. */
 DWT2D_B200_API int dwt2d_plan_set_tuning(dwt2d_plan* plan, const char* name, int value);

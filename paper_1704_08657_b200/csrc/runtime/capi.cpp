@@ -40,6 +40,8 @@ struct Tuning {
   int crop_core = 12;       // DWT2D_CROP_CORE: positions per crop tile (capped by the crop kernel's 256 cells)
   int host_band_rows = 0;   // DWT2D_HOST_BAND_ROWS: image rows per host pipeline band (0: policy)
   int host_levels = 0;      // DWT2D_HOST_LEVELS: levels pipelined by bands in the host entry point (0: policy)
+  int host_taper = 0;       // DWT2D_HOST_TAPER: 1 = short first and last host pipeline bands
+  int host_trace = 0;       // DWT2D_HOST_TRACE: 1 = print the host pipeline's timeline (development)
 };
 
 namespace {
@@ -59,6 +61,8 @@ Tuning tuning_from_env() {
   t.crop_core = std::max(1, env_int("DWT2D_CROP_CORE", t.crop_core));
   t.host_band_rows = env_int("DWT2D_HOST_BAND_ROWS", t.host_band_rows);
   t.host_levels = env_int("DWT2D_HOST_LEVELS", t.host_levels);
+  t.host_taper = env_int("DWT2D_HOST_TAPER", t.host_taper);
+  t.host_trace = env_int("DWT2D_HOST_TRACE", t.host_trace);
   return t;
 }
 }  // namespace
@@ -1372,6 +1376,31 @@ struct HostPipe {
     cuda_check(cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking), "stream");
   }
+  // timeline trace (tuning host_trace; development only): timing events
+  // recorded on the pipeline's streams, printed to stderr after the call
+  std::vector<cudaEvent_t> tev;
+  std::vector<std::string> tname;
+  size_t ntrace = 0;
+  void mark(bool on, cudaStream_t st, const std::string& name) {
+    if (!on) return;
+    if (tev.size() <= ntrace) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "event");
+      tev.push_back(e);
+      tname.emplace_back();
+    }
+    tname[ntrace] = name;
+    cuda_check(cudaEventRecord(tev[ntrace++], st), "record");
+  }
+  void dump(bool on) {
+    if (!on || ntrace == 0) return;
+    for (size_t i = 0; i < ntrace; ++i) {
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, tev[0], tev[i]), "elapsed");
+      std::fprintf(stderr, "[host_trace] %8.3f ms  %s\n", ms, tname[i].c_str());
+    }
+    ntrace = 0;
+  }
   cudaEvent_t event(size_t i) {
     while (ev.size() <= i) {
       cudaEvent_t e;
@@ -1391,22 +1420,41 @@ HostPipe& host_pipe() {
   return *p;
 }
 
-// Row bands of the host pipeline: `n` bands of `rows` image rows, the last
-// band taking the remainder (rows <= last < 2 * rows), so every band —
-// including the last — is at least `rows` >= 4 * halo rows tall and each
-// band's bottom halo lies inside the next band (or wraps to row 0).
+// Row bands of the host pipeline: bands of `rows` image rows, the last one
+// taking the remainder (rows <= last < 2 * rows), so every band — including
+// the last — is at least `rows` >= 4 * halo rows tall. Tapered (tuning
+// host_taper): the first band is rows / 4 tall (the D2H stream starts
+// sooner) and the last `rows` rows are split rows / 2, rows / 4, rows / 4
+// (less is left to copy down after the last upload).
 struct Bands {
-  int rows, n;
-  int begin(int b) const { return b * rows; }
-  int end(int b, int H) const { return b == n - 1 ? H : (b + 1) * rows; }
+  std::vector<int> edge;  // band b = image rows [edge[b], edge[b + 1])
+  int n = 0;
+  int begin(int b) const { return edge[b]; }
+  int end(int b, int) const { return edge[b + 1]; }
 };
 Bands bands_for(const dwt2d_plan& p, int H, int halo_rows) {
   int r = p.tune.host_band_rows;
   if (r <= 0) r = H / 16;                         // ~16 bands
-  r = std::max(r, std::max(64, 4 * halo_rows));   // level-2 bands need their own halo rows
+  const int lo = std::max(64, 4 * halo_rows);     // level-2 bands need their own halo rows
+  r = std::max(r, lo);
   r = (r + 3) & ~3;                               // even LL1 rows per band
   r = std::min(r, H);
-  return Bands{r, std::max(1, H / r)};
+  const int n = std::max(1, H / r);
+  Bands b;
+  for (int i = 0; i < n; ++i) b.edge.push_back(i * r);
+  b.edge.push_back(H);
+  const int q = (r / 4) & ~3;
+  if (p.tune.host_taper && n >= 3 && q >= lo && q <= H - 4 * q - lo) {
+    // the first band split q + (r - q), the last 4q rows 2q + q + q; the
+    // band before them absorbs the remainder (at least lo rows)
+    std::vector<int> e{0, q};
+    for (int i = 1; i < n; ++i)
+      if (i * r <= H - 4 * q - lo) e.push_back(i * r);
+    for (const int t : {H - 4 * q, H - 2 * q, H - q, H}) e.push_back(t);
+    b.edge = e;
+  }
+  b.n = int(b.edge.size()) - 1;
+  return b;
 }
 
 // One forward level on image rows [r0, r1) of a level input `in` (w_in x
@@ -1523,6 +1571,8 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
   auto inp_of = [&](int l) { return l == 1 ? size_t(W) : llp(l - 1); };
 
   size_t ev = 0;
+  const bool tr = p.tune.host_trace != 0;
+  hp.mark(tr, hp.comp, "start");
   cudaEvent_t ev_alloc = hp.event(ev++);
   cuda_check(cudaEventRecord(ev_alloc, hp.comp), "record");
   cuda_check(cudaStreamWaitEvent(hp.up, ev_alloc), "wait");
@@ -1543,6 +1593,7 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
                  "H2D");
     up[b] = hp.event(ev++);
     cuda_check(cudaEventRecord(up[b], hp.up), "record");
+    hp.mark(tr, hp.up, "up " + std::to_string(b));
   }
 
   auto down_after = [&](auto&& copy) {
@@ -1554,7 +1605,9 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
   auto level_band = [&](int l, int b) {
     const int wl = W >> (l - 1), hl = H >> (l - 1), r0 = C[l - 1][b], r1 = C[l - 1][b + 1];
     band_level(p, in_of(l), inp_of(l), wl, hl, r0, r1, ll(l), llp(l), d_out, size_t(W), hp.comp);
+    hp.mark(tr, hp.comp, "comp L" + std::to_string(l) + " b" + std::to_string(b));
     down_after([&] { band_details_down(out, d_out, W, wl, hl, r0 / 2, (r1 - r0) / 2, hp.down); });
+    hp.mark(tr, hp.down, "down L" + std::to_string(l) + " b" + std::to_string(b));
   };
 
   for (int b = 0; b < B; ++b) {
@@ -1568,12 +1621,15 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     }
   }
   if (levels > P) forward_mallat(p, ll(P), llp(P), wP, hP, levels - P, d_out, size_t(W), d_sub, hp.comp);
+  hp.mark(tr, hp.comp, "comp deep levels");
   down_after([&] {  // the remaining top-left corner (levels > P and LL_levels)
     cuda_check(cudaMemcpy2DAsync(out, size_t(W) * 4, d_out, size_t(W) * 4, size_t(wP) * 4, hP,
                                  cudaMemcpyDeviceToHost, hp.down),
                "D2H");
   });
+  hp.mark(tr, hp.down, "down quadrant");
   cuda_check(cudaStreamSynchronize(hp.down), "synchronize");
+  hp.dump(tr);
 }
 
 }  // namespace
@@ -1655,6 +1711,8 @@ int dwt2d_plan_set_tuning(dwt2d_plan* p, const char* name, int value) {
     else if (n == "crop_core") t.crop_core = std::max(1, value);
     else if (n == "host_band_rows") t.host_band_rows = value;
     else if (n == "host_levels") t.host_levels = value;
+    else if (n == "host_taper") t.host_taper = value;
+    else if (n == "host_trace") t.host_trace = value;
     else fail(DWT2D_EINVAL, "unknown tuning switch: " + n);
   });
 }

@@ -283,17 +283,20 @@ def test_bottom_up_chunks_bit_exact(dwt, cuda, w, s, opt, monkeypatch):
             assert torch.equal(fa[j], fb[j]), (chunk, j)
 
 
-@pytest.mark.parametrize("host_levels", [0, 1, 2])
+@pytest.mark.parametrize("taper", [0, 1])
+@pytest.mark.parametrize("host_levels", [0, 1, 3])
 @pytest.mark.parametrize("band_rows", ["0", "64", "96", "10000"])
-def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, host_levels):
+def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, host_levels, taper):
     """The pipelined host entry point (row bands uploaded while the first
     levels run band by band on earlier bands, compute bands trailing the
     upload bands by the bottom halo, LL tails computed early for band 0's
     periodic top halo) equals the device pyramid bit for bit, for several
-    band splits incl. a ragged last band and 1, 2 or 3 pipelined levels."""
+    band splits incl. a ragged last band, 1, 2 or 3 pipelined levels, and
+    tapered bands (short first and last bands)."""
     import torch
     plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True).tune(host_band_rows=int(band_rows),
-                                                                           host_levels=host_levels)
+                                                                           host_levels=host_levels,
+                                                                           host_taper=taper)
     # H = 1026 / 1028: the default bands leave a 2-row remainder, which the
     # last band absorbs (a 2-row band would be thinner than its halo)
     # and deeper pyramids: exactly 3 levels, more levels, a single band, a
