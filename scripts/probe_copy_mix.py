@@ -19,6 +19,8 @@ dimg = torch.empty(n, dtype=torch.float32, device="cuda")
 dout = torch.empty(n, dtype=torch.float32, device="cuda")
 up = torch.cuda.Stream()
 down = torch.cuda.Stream()
+up2 = torch.cuda.Stream()
+down2 = torch.cuda.Stream()
 import ctypes
 from pathlib import Path
 zc = ctypes.CDLL(str(Path(__file__).resolve().parents[1] / "build/probe_zcopy.so"))
@@ -39,13 +41,31 @@ def run(mode):
     t0 = time.perf_counter()
     for b in range(B):
         o = b * rows * W * 4
-        ck(rt.cudaMemcpyAsync(dimg.data_ptr() + o, himg.data_ptr() + o, rows * W * 4, H2D, up.cuda_stream))
-        evs[b].record(up)
+        us = up2 if (mode.endswith("x2") and b % 2) else up
+        if mode.endswith("h2"):  # each band's upload split over two streams
+            half = rows * W * 2
+            ck(rt.cudaMemcpyAsync(dimg.data_ptr() + o, himg.data_ptr() + o, half, H2D, up.cuda_stream))
+            ck(rt.cudaMemcpyAsync(dimg.data_ptr() + o + half, himg.data_ptr() + o + half, half, H2D, up2.cuda_stream))
+            up.wait_stream(up2)
+            us = up
+        else:
+            ck(rt.cudaMemcpyAsync(dimg.data_ptr() + o, himg.data_ptr() + o, rows * W * 4, H2D, us.cuda_stream))
+        evs[b].record(us)
     w2, h2, hb = W // 2, H // 2, rows // 2
     for b in range(B):
-        down.wait_event(evs[b])
+        ds = down2 if (mode.endswith("x2") and b % 2) else down
+        ds.wait_event(evs[b])
         y0 = b * hb
         if mode == "none":
+            continue
+        if mode.startswith("1d") and (mode.endswith("x2") or mode.endswith("h2")):
+            o1 = (y0 * W) * 4
+            ck(rt.cudaMemcpyAsync(hout.data_ptr() + o1, dout.data_ptr() + o1, hb * w2 * 4, D2H, ds.cuda_stream))
+            o2 = ((h2 + y0) * W) * 4
+            s2 = down2 if mode.endswith("h2") else ds
+            if mode.endswith("h2"):
+                s2.wait_event(evs[b])
+            ck(rt.cudaMemcpyAsync(hout.data_ptr() + o2, dout.data_ptr() + o2, hb * W * 4, D2H, s2.cuda_stream))
             continue
         if mode == "2d":
             o1 = (y0 * W + w2) * 4
@@ -70,6 +90,19 @@ def run(mode):
     return (time.perf_counter() - t0) * 1e3
 
 
+def both_big():
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ck(rt.cudaMemcpyAsync(dimg.data_ptr(), himg.data_ptr(), n * 4, H2D, up.cuda_stream))
+    ck(rt.cudaMemcpyAsync(hout.data_ptr(), dout.data_ptr(), n * 3, D2H, down.cuda_stream))
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t0) * 1e3
+
+
+ts = sorted(both_big() for _ in range(5))
+print(f"one 1 GiB H2D + one 768 MB D2H, concurrent: median {ts[2]:.2f} ms", flush=True)
+
+
 # D2H alone through each mechanism (768 MB)
 def d2h_only(mode):
     torch.cuda.synchronize()
@@ -86,6 +119,6 @@ for mode in ["ce", "kernel", "ce", "kernel"]:
     ts = sorted(d2h_only(mode) for _ in range(5))
     print(f"D2H only {mode:6s} 768 MB median {ts[2]:7.2f} ms ({0.805306368e3 / ts[2]:.1f} GB/s)", flush=True)
 hout.copy_(dout.cpu())
-for mode in ["none", "2d", "1d", "kernel", "2d", "kernel", "none"]:
+for mode in ["none", "1d", "1dx2", "1dh2", "1d", "1dx2", "1dh2"]:
     ts = sorted(run(mode) for _ in range(5))
     print(f"{mode:5s} median {ts[2]:7.2f} ms  min {ts[0]:7.2f} ms", flush=True)
