@@ -1515,7 +1515,9 @@ void band_details_down(float* hdet, const float* det, int W, int w_in, int h_in,
 // level l, T_P = 2 up); the last band recomputes those rows with identical
 // values. Levels P+1.. run on the device-resident LL_P, and only its
 // quadrant goes down last.
-void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int W, int H, int levels,
+// Returns false (nothing enqueued) when the image is too short for even one
+// band and its halos; the caller then copies it whole.
+bool forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int W, int H, int levels,
                                    float* out) {
   HostPipe& hp = host_pipe();
   const int U = p.up, Ld = p.down;
@@ -1549,7 +1551,7 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
     ok = ok && T[0] + 2 * Ld <= H;
     if (ok || P == 1) break;
   }
-  if (T[0] + 2 * Ld > H) fail(DWT2D_EINVAL, "image smaller than the level halo");
+  if (T[0] + 2 * Ld > H) return false;
 
   // device buffers: image, Mallat output, LL_1 .. LL_P (LL_levels goes into
   // the output), workspace of the device-resident levels
@@ -1630,6 +1632,7 @@ void forward_mallat_host_pipelined(const dwt2d_plan& p, const float* image, int 
   hp.mark(tr, hp.down, "down quadrant");
   cuda_check(cudaStreamSynchronize(hp.down), "synchronize");
   hp.dump(tr);
+  return true;
 }
 
 }  // namespace
@@ -2433,9 +2436,7 @@ int dwt2d_forward_mallat_host(const dwt2d_plan* p, const float* image, int W, in
     if (!p->forward) fail(DWT2D_EINVAL, "forward_mallat: plan is an inverse plan");
     check_pyramid(W, H, levels);
     if (is_identity(*p)) fail(DWT2D_EUNSUPPORTED, "identity program");
-    if (p->entry && p->extension == DWT2D_PERIODIC) {
-      forward_mallat_host_pipelined(*p, image, W, H, levels, out);
-    } else {
+    if (!(p->entry && p->extension == DWT2D_PERIODIC && forward_mallat_host_pipelined(*p, image, W, H, levels, out))) {
       HostPipe& hp = host_pipe();
       const size_t n = size_t(W) * H;
       const size_t ws_bytes = dwt2d_workspace_bytes(W, H, levels);

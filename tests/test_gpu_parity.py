@@ -309,6 +309,18 @@ def test_host_pipeline_bands_bit_exact(dwt, cuda, band_rows, host_levels, taper)
         assert np.array_equal(dev, host), (band_rows, W, H, L)
 
 
+def test_host_entry_point_tiny_images(dwt, cuda):
+    """Images shorter than one host-pipeline band and its halos go up whole
+    (no band pipeline) and still equal the device pyramid bit for bit."""
+    import torch
+    plan = dwt.Plan("cdf97", "nonseparable-lifting", optimized=True)
+    for W, H, L in [(8, 8, 3), (16, 4, 2), (64, 8, 1), (32, 16, 4)]:
+        img = O.random_image(W, H, 5)
+        dev = plan.forward_mallat(torch.from_numpy(img).to(cuda), L).cpu().numpy()
+        host = plan.forward_mallat_host(img, L)
+        assert np.array_equal(dev, host), (W, H, L)
+
+
 def test_pitched_and_offset_views(dwt, cuda):
     """Row pitch != width and misaligned sub-views use the scalar path and
     agree with the dense vector path."""
