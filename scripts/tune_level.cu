@@ -5,6 +5,7 @@
 //        --expt-relaxed-constexpr -I include scripts/tune_level.cu -o build/tune_level
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "../paper_1704_08657_b200/csrc/generated/plans_gen.cuh"
@@ -39,7 +40,7 @@ void run(const char* name, float* img, float* out[4], int W, int H, int chunk, c
   a.vec = 1;
   const long long warps = (long long)a.nstrips * a.nchunks;
   const unsigned blocks = unsigned((warps + kWarpsPerCta - 1) / kWarpsPerCta);
-  auto k = level_kernel<Pl, PF, true, false, true, MINB>;
+  auto k = level_kernel<Pl, PF, true, false, true, false, MINB>;
   cudaFuncAttributes fa;
   CK(cudaFuncGetAttributes(&fa, k));
   for (int i = 0; i < 3; ++i) k<<<blocks, 128>>>(a);
@@ -76,6 +77,20 @@ int main(int argc, char** argv) {
   const size_t n = size_t(W / 2) * (H / 2);
   std::vector<float> ref(n), host(n);
   using P = plans::cdf97_nonseparable_lifting_opt;
+  if (argc > 1 && std::string(argv[1]) == "mid") {
+    // mid-size levels (BASELINE configs[1], pyramid level 3/4 inputs):
+    // resident CTAs per SM (registers) x prefetch depth x chunk rows
+    for (int sz : {4096, 2048}) {
+      for (int chunk : {8, 12, 16, 22, 32}) {
+        run<WithCW<P, 4>, 2, 1>("cw4 pf2", img, out, sz, sz, chunk, nullptr, nullptr);
+        run<WithCW<P, 4>, 2, 4>("cw4 pf2 minb4", img, out, sz, sz, chunk, nullptr, nullptr);
+        run<WithCW<P, 4>, 3, 4>("cw4 pf3 minb4", img, out, sz, sz, chunk, nullptr, nullptr);
+        run<WithCW<P, 2>, 2, 4>("cw2 pf2 minb4", img, out, sz, sz, chunk, nullptr, nullptr);
+        run<WithCW<P, 2>, 4, 4>("cw2 pf4 minb4", img, out, sz, sz, chunk, nullptr, nullptr);
+      }
+    }
+    return 0;
+  }
   for (int sz : {2048, 1024, 512, 256, 128}) {
     for (int chunk : {2, 4, 8}) {
       run<WithCW<P, 4>, 2, 1>("cw4 pf2", img, out, sz, sz, chunk, nullptr, nullptr);
