@@ -339,6 +339,36 @@ def run_single(args, plan, img, out, dev):
             "launches": launches, "clk": clk}
 
 
+def c4_on_one_gpu(plan, dev, steps=5):
+    """configs[4]'s 65536^2 image as one 8-level pyramid on this one GPU
+    (37 GiB resident): the same-workload single-GPU rate that the N > 1
+    lines (65536^2 strong-scaled over N GPUs) scale from. Not part of the
+    N = 1 timed region."""
+    import torch
+    import paper_1704_08657_b200 as dwt
+    from paper_1704_08657_b200.synth import random_image
+    size = WORKLOADS["c4"][0]
+    img = random_image(size, size, 1, device=dev)
+    out = torch.empty_like(img)
+    scratch = torch.empty(dwt.workspace_bytes(size, size, LEVELS) // 4 + 64, dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            plan.forward_mallat(img, LEVELS, out=out, scratch=scratch, stream=stream.cuda_stream)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            plan.forward_mallat(img, LEVELS, out=out, scratch=scratch, stream=stream.cuda_stream)
+        t1.record(stream)
+        t1.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    del img, out, scratch
+    torch.cuda.empty_cache()
+    return {"value": size * size / (ms * 1e-3) / 1e9, "unit": "Gpixel/s", "ms_per_step": ms, "steps": steps,
+            "workload": f"{size}x{size} float32, {LEVELS} levels on one GPU (BASELINE configs[4]'s image): the "
+                        "single-GPU rate of the workload the N > 1 lines strong-scale"}
+
+
 def run_sharded(args, plan, shard, img, out, dev, n):
     """N > 1: every rank's strip pyramid (dwt2d_shard_forward_mallat: halo
     pushes into the ring neighbours' windows, interior rows, device-side
@@ -420,6 +450,8 @@ def main():
     ap.add_argument("--workload", default="auto", choices=["auto", "c3", "c4"],
                     help="c3: 16384^2 (BASELINE configs[3]), c4: 65536^2 (configs[4]); auto: c3 at N=1, c4 at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4-reference", action="store_true",
+                    help="N = 1: skip the 65536^2 single-GPU pyramid reported next to the headline")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--sharded", action="store_true",
                     help="run the N>1 sharded path (ring of one at N=1; testing)")
@@ -519,6 +551,12 @@ def main():
                        "8 B/pixel/level algorithmic" if r["fused12"] else
                        f"level 1 ({W}x{Hs}), 8 B/pixel algorithmic")
         pyr_bytes = sum(8.0 * (W >> l) * (Hs >> l) for l in range(LEVELS))
+        c4_ref = None
+        if n == 1 and not sharded and wl == "c3" and not args.no_c4_reference:
+            try:
+                c4_ref = c4_on_one_gpu(plan, dev)
+            except Exception as e:  # e.g. not enough free device memory
+                c4_ref = {"value": None, "unavailable": str(e)[:200]}
         cpu = None
         if not args.no_cpu_baseline and n == 1:
             try:
@@ -553,6 +591,8 @@ def main():
             "clocks": r["clk"].summary(),
             "cpu_baseline": cpu,
         }
+        if c4_ref is not None:
+            line["c4_single_gpu"] = c4_ref
         if sharded:
             info = shard.info()
             line["halo_exchange"] = {
