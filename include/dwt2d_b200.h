@@ -345,7 +345,12 @@ DWT2D_B200_API int dwt2d_inverse_mallat(const dwt2d_plan* inverse_plan, const fl
  * executor.hpp:196-197): synchronous, returns when out[] is filled. */
 DWT2D_B200_API int dwt2d_run_planar_host(const dwt2d_plan* plan, const float* const in[4],
                                          float* const out[4], int w2, int h2);
-/* Mallat pyramid of a host image into a host buffer (both W x H, dense). */
+/* Mallat pyramid of a host image into a host buffer (both W x H, dense).
+ * Periodic plans with a fused kernel pipeline the copies: the image goes up
+ * in row bands while levels 1-2 run band by band and each band's detail rows
+ * go down; other plans, and images too short for a band and
+ * its halos, are copied whole. Synchronous. Pinned host memory gives full
+ * PCIe bandwidth. */
 DWT2D_B200_API int dwt2d_forward_mallat_host(const dwt2d_plan* plan, const float* image,
                                              int width, int height, int levels, float* out);
 DWT2D_B200_API int dwt2d_inverse_mallat_host(const dwt2d_plan* inverse_plan, const float* in,
